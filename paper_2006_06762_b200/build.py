@@ -1,0 +1,76 @@
+"""Build the native library in-tree: nvcc for sm_100a, one shared object.
+
+`python -m paper_2006_06762_b200.build` (or `__graft_entry__.build()`) writes
+`paper_2006_06762_b200/_lib/libloomtune_b200.so` plus the NVRTC compile worker
+`paper_2006_06762_b200/_lib/lt_nvrtc_worker`.  Objects are rebuilt only when a
+source is newer than its output.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIBDIR = os.path.join(HERE, "_lib")
+LIB = os.path.join(LIBDIR, "libloomtune_b200.so")
+WORKER = os.path.join(LIBDIR, "lt_nvrtc_worker")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+# exact-arithmetic kernels must not contract a*b+c into an FMA
+SOURCES = {
+    "features.cu": ["--fmad=false"],
+    "predict.cu": ["--fmad=false"],
+    "api.cu": [],
+    "runner.cu": [],
+    "compile_pool.cpp": [],
+}
+
+
+def _stale(out: str, deps: list) -> bool:
+    if not os.path.exists(out):
+        return True
+    t = os.path.getmtime(out)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list) -> None:
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"build failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(LIBDIR, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
+    objs = []
+    for src, extra in SOURCES.items():
+        path = os.path.join(CSRC, src)
+        if not os.path.exists(path):
+            continue
+        obj = os.path.join(LIBDIR, src.rsplit(".", 1)[0] + ".o")
+        objs.append(obj)
+        if _stale(obj, [path] + headers + [__file__]):
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                   "-I", CSRC, "-I", os.path.join(CUDA, "include"), *extra, "-c", path, "-o", obj]
+            if src.endswith(".cpp"):
+                cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, *extra, "-c", path, "-o", obj]
+            if verbose:
+                print(" ".join(cmd))
+            _run(cmd)
+    if _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", os.path.join(CUDA, "lib64"), "-lcudart",
+              "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")])
+    wsrc = os.path.join(CSRC, "nvrtc_worker.cpp")
+    if os.path.exists(wsrc) and _stale(WORKER, [wsrc] + headers):
+        _run(["g++", "-O2", "-std=c++17", "-I", os.path.join(CUDA, "include"), wsrc, "-o", WORKER,
+              "-L", os.path.join(CUDA, "lib64"), "-lnvrtc", "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,420 @@
+// Batched per-statement feature extraction on sm_100a.
+//
+// Replaces `extract_features` / `analyze_program` / `statement_features`
+// (reference src/features.py:161-425).  One thread per statement record (the
+// record format is produced by paper_2006_06762_b200/encode.py and documented in
+// include/loomtune_b200.h).  All structural resolution (attach chains, id-based
+// loop identity, first-access views, packing strides, name ranks) is done by the
+// encoder; this kernel performs every interval / evaluation / product the
+// reference does, in the same order and with the same fp64 rounding:
+//   * decode-AST intervals with the DMod same-block rule (src/ir.py:122-149),
+//     floor division semantics of Python for negative operands;
+//   * hull widths, unique bytes/lines, reuse classification, strides, working
+//     sets (src/features.py:143-158,202-274);
+//   * annotation / unroll blocks, intensity curve, ranked buffer blocks,
+//     log2(1+max(x,0)) compression (src/features.py:296-417).
+// Compiled with --fmad=false so no product/sum pair is contracted into an FMA.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+#include "common.h"
+
+namespace lt {
+
+constexpr int HDR = 18;
+constexpr int NF = 164;
+constexpr int MAX_NEST = 32;
+constexpr int MAX_LOOPS = 64;
+constexpr int MAX_ITERS = 24;
+constexpr int MAX_VIEWS = 12;
+constexpr int MAX_STACK = 48;
+
+struct Iv { long long lo, hi; };
+
+__device__ __forceinline__ long long fdiv(long long a, long long c) {
+  long long q = a / c;
+  if ((a % c != 0) && ((a < 0) != (c < 0))) --q;
+  return q;
+}
+__device__ __forceinline__ long long fmod_(long long a, long long c) {
+  long long r = a % c;
+  if (r != 0 && ((r < 0) != (c < 0))) r += c;
+  return r;
+}
+
+// interval of one postfix decode AST given per-own-loop upper bounds (lo = 0)
+__device__ bool ast_interval(const int32_t* nodes, int cnt, const long long* hi, Iv& out) {
+  Iv st[MAX_STACK];
+  int sp = 0;
+  for (int n = 0; n < cnt; ++n) {
+    int op = nodes[2 * n], arg = nodes[2 * n + 1];
+    switch (op) {
+      case 0: if (sp >= MAX_STACK) return false; st[sp].lo = 0; st[sp].hi = hi[arg]; ++sp; break;
+      case 1: if (sp >= MAX_STACK) return false; st[sp].lo = arg; st[sp].hi = arg; ++sp; break;
+      case 2: { if (sp < 2) return false; Iv b = st[--sp]; st[sp - 1].lo += b.lo; st[sp - 1].hi += b.hi; break; }
+      case 3: { if (sp < 1) return false; Iv a = st[sp - 1]; long long c = arg;
+                st[sp - 1] = c >= 0 ? Iv{a.lo * c, a.hi * c} : Iv{a.hi * c, a.lo * c}; break; }
+      case 4: { if (sp < 1) return false; Iv a = st[sp - 1]; st[sp - 1] = Iv{fdiv(a.lo, arg), fdiv(a.hi, arg)}; break; }
+      case 5: { if (sp < 1) return false; Iv a = st[sp - 1];
+                if (fdiv(a.lo, arg) == fdiv(a.hi, arg)) st[sp - 1] = Iv{fmod_(a.lo, arg), fmod_(a.hi, arg)};
+                else st[sp - 1] = Iv{0, (long long)arg - 1};
+                break; }
+      default: return false;
+    }
+  }
+  if (sp != 1) return false;
+  out = st[0];
+  return true;
+}
+
+__device__ bool ast_eval(const int32_t* nodes, int cnt, const long long* env, long long& out) {
+  long long st[MAX_STACK];
+  int sp = 0;
+  for (int n = 0; n < cnt; ++n) {
+    int op = nodes[2 * n], arg = nodes[2 * n + 1];
+    switch (op) {
+      case 0: if (sp >= MAX_STACK) return false; st[sp++] = env[arg]; break;
+      case 1: if (sp >= MAX_STACK) return false; st[sp++] = arg; break;
+      case 2: if (sp < 2) return false; --sp; st[sp - 1] += st[sp]; break;
+      case 3: if (sp < 1) return false; st[sp - 1] *= arg; break;
+      case 4: if (sp < 1) return false; st[sp - 1] = fdiv(st[sp - 1], arg); break;
+      case 5: if (sp < 1) return false; st[sp - 1] = fmod_(st[sp - 1], arg); break;
+      default: return false;
+    }
+  }
+  if (sp != 1) return false;
+  out = st[0];
+  return true;
+}
+
+struct View {
+  const int32_t* dims;   // -> first dim record
+  int n_marks, has_w, rank, n_dims;
+  unsigned long long present;  // bitmask over own loops
+};
+
+// next dim record: (size, st, pext, const, n_terms, (it, c) * n_terms)
+__device__ __forceinline__ const int32_t* dim_next(const int32_t* d) { return d + 5 + 2 * d[4]; }
+
+__device__ __forceinline__ Iv dim_interval(const int32_t* d, const Iv* iv) {
+  long long lo = d[3], hi = d[3];
+  for (int t = 0; t < d[4]; ++t) {
+    int it = d[5 + 2 * t];
+    long long c = d[6 + 2 * t];
+    if (c >= 0) { lo += c * iv[it].lo; hi += c * iv[it].hi; }
+    else { lo += c * iv[it].hi; hi += c * iv[it].lo; }
+  }
+  int st = d[1], pext = d[2];
+  if (pext > 0) {
+    if (st > 1) { lo = fdiv(lo, st); hi = fdiv(hi, st); }
+    if (fdiv(lo, pext) == fdiv(hi, pext)) { lo = fmod_(lo, pext); hi = fmod_(hi, pext); }
+    else { lo = 0; hi = pext - 1; }
+  }
+  return Iv{lo, hi};
+}
+
+__device__ __forceinline__ long long dim_value(const int32_t* d, const long long* val) {
+  long long v = d[3];
+  for (int t = 0; t < d[4]; ++t) v += (long long)d[6 + 2 * t] * val[d[5 + 2 * t]];
+  int st = d[1], pext = d[2];
+  if (pext > 0) {
+    if (st > 1) v = fdiv(v, st);
+    v = fmod_(v, pext);
+  }
+  return v;
+}
+
+__device__ __forceinline__ long long hull_width(const int32_t* d, const Iv* iv) {
+  Iv r = dim_interval(d, iv);
+  long long size = d[0];
+  long long lo = r.lo > 0 ? r.lo : 0;
+  long long hi = r.hi < size - 1 ? r.hi : size - 1;
+  long long w = hi - lo + 1;
+  return w > 1 ? w : 1;
+}
+
+// position tag of nest entry i among same-kind loops (src/features.py:296-305)
+__device__ int position(const int32_t* nest, int n_nest, int i) {
+  int kind = nest[4 * i + 1];
+  int cnt = 0, rank = 0;
+  for (int j = 0; j < n_nest; ++j)
+    if (nest[4 * j + 1] == kind) { if (j < i) ++rank; ++cnt; }
+  int base = kind == 0 ? 1 : 4;                 // inner_spatial / inner_reduce
+  if (rank == cnt - 1) return base;
+  if (rank == 0 && cnt > 1) return base + 2;    // outer
+  return base + 1;                              // middle
+}
+
+struct Row {
+  double* v;
+  __device__ void set(int i, double x) { v[i] = x; }
+};
+
+__device__ void annotation_block(const int32_t* nest, int n_nest, int ann, double* b) {
+  for (int i = 0; i < 11; ++i) b[i] = 0.0;
+  int hits = 0, last = -1, tag = -1;
+  double prod = 1.0;
+  for (int i = 0; i < n_nest; ++i) {
+    if (nest[4 * i + 2] != ann) continue;
+    int p = position(nest, n_nest, i);
+    tag = (hits == 0) ? p : (tag == p ? tag : 7);
+    prod *= (double)nest[4 * i];
+    last = i;
+    ++hits;
+  }
+  if (!hits) { b[1] = 1.0; return; }
+  b[0] = (double)nest[4 * last];
+  b[1 + tag] = 1.0;
+  b[9] = prod;
+  b[10] = (double)hits;
+}
+
+__global__ void __launch_bounds__(128)
+features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off,
+                int64_t n_stmt, double* __restrict__ rows, int* __restrict__ err) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_stmt) return;
+  const int32_t* r = words + stmt_off[s];
+  double* out = rows + s * NF;
+
+  const int n_nest = r[0], own_start = r[1], n_loops = r[2], n_iter = r[3], n_views = r[4];
+  const int unroll = r[5], n_live = r[6], has_reduce = r[7];
+  const int32_t* ops = r + 8;
+  const int n_nodes = r[17];
+  if (n_nest > MAX_NEST || n_loops > MAX_LOOPS || n_iter > MAX_ITERS || n_views > MAX_VIEWS) {
+    for (int i = 0; i < NF; ++i) out[i] = __longlong_as_double(0x7ff8000000000000ULL);
+    atomicExch(err, 1);
+    return;
+  }
+  const int32_t* nest = r + HDR;
+  const int32_t* loops = nest + 4 * n_nest;
+  const int32_t* itab = loops + 3 * n_loops;
+  const int32_t* nodes = itab + 2 * n_iter;
+  const int32_t* vp = nodes + 2 * n_nodes;
+
+  View views[MAX_VIEWS];
+  unsigned long long iter_mask[MAX_ITERS];
+  for (int it = 0; it < n_iter; ++it) {
+    unsigned long long m = 0;
+    const int32_t* nd = nodes + 2 * itab[2 * it];
+    for (int n = 0; n < itab[2 * it + 1]; ++n)
+      if (nd[2 * n] == 0) m |= 1ULL << nd[2 * n + 1];
+    iter_mask[it] = m;
+  }
+  for (int v = 0; v < n_views; ++v) {
+    View& w = views[v];
+    w.n_marks = vp[0]; w.has_w = vp[1]; w.rank = vp[2]; w.n_dims = vp[3];
+    w.dims = vp + 4;
+    const int32_t* d = w.dims;
+    unsigned long long m = 0;
+    for (int k = 0; k < w.n_dims; ++k) {
+      for (int t = 0; t < d[4]; ++t) m |= iter_mask[d[5 + 2 * t]];
+      d = dim_next(d);
+    }
+    w.present = m;
+    vp = d;
+  }
+
+  // own-range intervals of every iterator decode
+  long long hi[MAX_LOOPS];
+  Iv iv[MAX_ITERS];
+  for (int j = 0; j < n_loops; ++j) hi[j] = (long long)loops[3 * j] - 1;
+  bool ok = true;
+  for (int it = 0; it < n_iter; ++it)
+    ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], hi, iv[it]);
+
+  double total = 1.0;
+  for (int i = 0; i < n_nest; ++i) total *= (double)nest[4 * i];
+  double red_prod = 1.0, alloc = 4.0;
+  for (int i = own_start; i < n_nest; ++i) {
+    if (nest[4 * i + 1] == 1) red_prod *= (double)nest[4 * i];
+    else alloc *= (double)nest[4 * i];
+  }
+  int ops_total = 0;
+  for (int k = 0; k < 9; ++k) ops_total += ops[k];
+
+  // per-view access statistics
+  double tb[MAX_VIEWS], ub[MAX_VIEWS], ul[MAX_VIEWS], cnt[MAX_VIEWS], di[MAX_VIEWS], db[MAX_VIEWS],
+      strd[MAX_VIEWS];
+  int acc[MAX_VIEWS], reuse[MAX_VIEWS];
+  const int inner_own = (n_nest > own_start) ? nest[4 * (n_nest - 1) + 3] : -1;
+  long long val0[MAX_ITERS], val1[MAX_ITERS];
+  if (inner_own >= 0) {
+    long long env[MAX_LOOPS];
+    for (int j = 0; j < n_loops; ++j) env[j] = 0;
+    for (int it = 0; it < n_iter; ++it) ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], env, val0[it]);
+    env[inner_own] = 1;
+    for (int it = 0; it < n_iter; ++it) ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], env, val1[it]);
+  }
+  for (int v = 0; v < n_views; ++v) {
+    const View& w = views[v];
+    const bool has_w = w.has_w != 0;
+    const bool has_r = (w.n_marks > w.has_w) || (has_w && red_prod > 1.0);
+    acc[v] = (has_w && has_r) ? 2 : (has_w ? 1 : 0);
+    long long uprod = 1, last = 1;
+    double lines = 1.0;
+    const int32_t* d = w.dims;
+    for (int k = 0; k < w.n_dims; ++k) {
+      long long wd = hull_width(d, iv);
+      uprod *= wd;
+      if (k < w.n_dims - 1) lines *= (double)wd; else last = wd;
+      d = dim_next(d);
+    }
+    ub[v] = (double)uprod * 4.0;
+    double lc = ceil((double)(last * 4) / 64.0);
+    ul[v] = lines * (lc > 1.0 ? lc : 1.0);
+    tb[v] = ((double)w.n_marks * total) * 4.0;
+    // reuse (src/features.py:224-242)
+    int absent_last = -1;
+    double counter = 1.0;
+    for (int i = 0; i < n_nest; ++i) {
+      int oi = nest[4 * i + 3];
+      bool present = oi >= 0 && ((w.present >> oi) & 1ULL);
+      if (!present && nest[4 * i] > 1) { counter *= (double)nest[4 * i]; absent_last = i; }
+    }
+    if (has_w && has_reduce && red_prod > 1.0) {
+      reuse[v] = 1; cnt[v] = red_prod; di[v] = 1.0; db[v] = (double)(4 * w.n_marks);
+    } else if (absent_last >= 0) {
+      reuse[v] = 0; cnt[v] = counter;
+      double dit = 1.0;
+      for (int i = absent_last + 1; i < n_nest; ++i) dit *= (double)nest[4 * i];
+      di[v] = dit; db[v] = (dit * 4.0) * (double)w.n_marks;
+    } else {
+      reuse[v] = 2; cnt[v] = 1.0; di[v] = 0.0; db[v] = 0.0;
+    }
+    // stride (src/features.py:244-259)
+    strd[v] = 0.0;
+    if (inner_own >= 0 && ((w.present >> inner_own) & 1ULL)) {
+      long long a0 = 0, a1 = 0, fs = 1;
+      // dims are walked inner->outer for row-major flat strides
+      const int32_t* dd[16];
+      const int32_t* q = w.dims;
+      int nd = w.n_dims < 16 ? w.n_dims : 16;
+      for (int k = 0; k < nd; ++k) { dd[k] = q; q = dim_next(q); }
+      for (int k = nd - 1; k >= 0; --k) {
+        long long size = dd[k][0];
+        long long x0 = dim_value(dd[k], val0), x1 = dim_value(dd[k], val1);
+        x0 = x0 < 0 ? 0 : (x0 > size - 1 ? size - 1 : x0);
+        x1 = x1 < 0 ? 0 : (x1 > size - 1 ? size - 1 : x1);
+        a0 += x0 * fs; a1 += x1 * fs;
+        fs *= size;
+      }
+      long long dlt = a1 - a0;
+      strd[v] = (double)((dlt < 0 ? -dlt : dlt) * 4);
+    }
+  }
+
+  // working set inside each nest position (src/features.py:266-274)
+  double ws[MAX_NEST];
+  for (int pos = 0; pos < n_nest; ++pos) {
+    long long h2[MAX_LOOPS];
+    Iv iv2[MAX_ITERS];
+    for (int j = 0; j < n_loops; ++j) h2[j] = loops[3 * j + 2] > pos ? (long long)loops[3 * j] - 1 : 0;
+    for (int it = 0; it < n_iter; ++it)
+      ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], h2, iv2[it]);
+    double acc_ws = 0.0;
+    for (int v = 0; v < n_views; ++v) {
+      long long p = 1;
+      const int32_t* d = views[v].dims;
+      for (int k = 0; k < views[v].n_dims; ++k) { p *= hull_width(d, iv2); d = dim_next(d); }
+      acc_ws += (double)p * 4.0;
+    }
+    ws[pos] = acc_ws;
+  }
+
+  // ---- row assembly (src/features.py:388-417) ----
+  double b[11];
+  for (int k = 0; k < 9; ++k) out[k] = (double)ops[k] * total;
+  for (int k = 9; k < 18; ++k) out[k] = 0.0;
+  annotation_block(nest, n_nest, 2, b);
+  for (int k = 0; k < 11; ++k) out[18 + k] = b[k];
+  {  // unroll block
+    for (int k = 0; k < 11; ++k) b[k] = 0.0;
+    long long prod = 1;
+    int n_cov = 0, first = -1, tag = -1;
+    if (unroll > 0 && n_nest > own_start) {
+      for (int i = n_nest - 1; i >= own_start; --i) {
+        if (prod * nest[4 * i] > unroll) break;
+        prod *= nest[4 * i];
+        int p = position(nest, n_nest, i);
+        tag = (n_cov == 0) ? p : (tag == p ? tag : 7);
+        if (n_cov == 0) first = i;
+        ++n_cov;
+      }
+    }
+    if (!n_cov) b[1] = 1.0;
+    else { b[0] = (double)nest[4 * first]; b[1 + tag] = 1.0; b[9] = (double)prod; b[10] = (double)n_cov; }
+    for (int k = 0; k < 11; ++k) out[29 + k] = b[k];
+  }
+  annotation_block(nest, n_nest, 1, b);
+  for (int k = 0; k < 11; ++k) out[40 + k] = b[k];
+  for (int k = 51; k < 59; ++k) out[k] = 0.0;
+  if (n_nest == 0 || ops_total == 0) {
+    for (int k = 59; k < 69; ++k) out[k] = 0.0;
+  } else {
+    double inside[MAX_NEST + 1];
+    inside[n_nest] = 1.0;
+    for (int i = n_nest - 1; i >= 0; --i) inside[i] = inside[i + 1] * (double)nest[4 * i];
+    for (int j = 1; j <= 10; ++j) {
+      int depth = (int)ceil((double)j / 10.0 * (double)n_nest);
+      if (depth < 1) depth = 1;
+      int pos = n_nest - depth;
+      double by;
+      if (pos == 0) { by = 0.0; for (int v = 0; v < n_views; ++v) by += ub[v]; }
+      else by = ws[pos - 1];
+      double flops = (double)ops_total * inside[pos];
+      out[58 + j] = flops / (by > 1.0 ? by : 1.0);
+    }
+  }
+  // ranked buffer blocks: by (-total_bytes, name)
+  bool used[MAX_VIEWS];
+  for (int v = 0; v < n_views; ++v) used[v] = false;
+  int n_rank = n_views < 5 ? n_views : 5;
+  for (int slot = 0; slot < 5; ++slot) {
+    double* o = out + 69 + 18 * slot;
+    if (slot >= n_rank) { for (int k = 0; k < 18; ++k) o[k] = 0.0; continue; }
+    int best = -1;
+    for (int v = 0; v < n_views; ++v) {
+      if (used[v]) continue;
+      if (best < 0 || tb[v] > tb[best] || (tb[v] == tb[best] && views[v].rank < views[best].rank)) best = v;
+    }
+    used[best] = true;
+    const int v = best;
+    for (int k = 0; k < 3; ++k) o[k] = (k == acc[v]) ? 1.0 : 0.0;
+    double ln = tb[v] / 64.0;
+    o[3] = tb[v]; o[4] = ub[v]; o[5] = ln; o[6] = ul[v];
+    for (int k = 0; k < 3; ++k) o[7 + k] = (k == reuse[v]) ? 1.0 : 0.0;
+    o[10] = di[v]; o[11] = db[v]; o[12] = cnt[v]; o[13] = strd[v];
+    double c = cnt[v] > 1.0 ? cnt[v] : 1.0;
+    o[14] = tb[v] / c; o[15] = ub[v] / c; o[16] = ln / c; o[17] = ul[v] / c;
+  }
+  out[159] = alloc;
+  out[160] = (double)n_live;
+  out[161] = (double)n_nest;
+  out[162] = total;
+  out[163] = (double)unroll;
+
+  // log2(1 + max(x, 0)) on every non-one-hot column
+  for (int k = 0; k < NF; ++k) {
+    if (is_onehot(k)) continue;
+    double x = out[k];
+    out[k] = log2(1.0 + (x > 0.0 ? x : 0.0));
+  }
+  if (!ok) {
+    for (int i = 0; i < NF; ++i) out[i] = __longlong_as_double(0x7ff8000000000000ULL);
+    atomicExch(err, 2);
+  }
+}
+
+}  // namespace lt
+
+extern "C" int lt_features_device(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt,
+                                  double* d_rows, int* d_err, void* stream) {
+  if (n_stmt <= 0) return 0;
+  const int threads = 128;
+  const int64_t blocks = (n_stmt + threads - 1) / threads;
+  lt::features_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(d_words, d_stmt_off, n_stmt,
+                                                                             d_rows, d_err);
+  return lt::check_launch("features_kernel");
+}

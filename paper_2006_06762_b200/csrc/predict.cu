@@ -1,0 +1,212 @@
+// GBDT inference over whole populations on sm_100a.
+//
+// Replaces `Tree.predict` / `CostModel.predict_rows` / `predict_matrix`
+// (reference src/model.py:75-108).  Exactness contract, matching numpy:
+//   * routing `x <= threshold` -> left, else right (NaN goes right), in fp64;
+//   * per row: acc = base, then acc += value[leaf] * eta tree by tree in list
+//     order (the product is precomputed on the host with the same IEEE multiply);
+//   * per program: numpy's add.reduce order over its rows (plain loop below 8
+//     rows, numpy's 8-accumulator pairwise scheme above).
+// Layout: the model's nodes live in global memory read through the read-only
+// path (61 KB at 30 trees x 127 nodes; L1-resident).  Each block stages a tile of
+// rows into shared memory with coalesced loads, restricted to the feature columns
+// the model actually tests, then each thread walks all trees for one row.
+// Compiled with --fmad=false.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <vector>
+#include <string>
+#include "common.h"
+
+namespace lt {
+
+constexpr int NF = 164;
+constexpr int ROWS_PER_BLOCK = 128;
+
+struct Node {
+  double x;        // threshold (internal) or value*eta (leaf)
+  int32_t feat;    // compact feature column, -1 at leaves
+  int32_t lr;      // left | right << 16 (tree-local node ids)
+};
+
+struct Model {
+  int n_trees = 0;
+  int n_used = 0;          // compact feature columns
+  double base = 0.0;
+  Node* d_nodes = nullptr;
+  int32_t* d_tree_off = nullptr;
+  int32_t* d_used = nullptr;   // compact col -> original feature index
+};
+
+__global__ void __launch_bounds__(ROWS_PER_BLOCK)
+predict_rows_kernel(const double* __restrict__ X, int64_t n_rows, const Node* __restrict__ nodes,
+                    const int32_t* __restrict__ tree_off, int n_trees, const int32_t* __restrict__ used,
+                    int n_used, double base, double* __restrict__ out) {
+  extern __shared__ double tile[];             // ROWS_PER_BLOCK x (n_used + 1)
+  const int ld = n_used + 1;                   // odd stride: conflict-free row access
+  const int64_t row0 = (int64_t)blockIdx.x * ROWS_PER_BLOCK;
+  const int rows_here = (int)min((int64_t)ROWS_PER_BLOCK, n_rows - row0);
+  for (int e = threadIdx.x; e < rows_here * n_used; e += blockDim.x) {
+    int r = e / n_used, c = e - r * n_used;
+    tile[r * ld + c] = X[(row0 + r) * NF + used[c]];
+  }
+  __syncthreads();
+  const int r = threadIdx.x;
+  if (r >= rows_here) return;
+  const double* x = tile + r * ld;
+  double acc = base;
+  for (int t = 0; t < n_trees; ++t) {
+    const Node* nd = nodes + tree_off[t];
+    Node cur = nd[0];
+    for (int lvl = 0; lvl < 64 && cur.feat >= 0; ++lvl) {
+      int nxt = (x[cur.feat] <= cur.x) ? (cur.lr & 0xffff) : (cur.lr >> 16);
+      cur = nd[nxt];
+    }
+    acc = __dadd_rn(acc, cur.x);
+  }
+  out[row0 + r] = acc;
+}
+
+// numpy pairwise_sum for float64 (numpy/_core/src/umath/loops_utils.h.src):
+// plain loop from +0.0 below 8 items, 8 accumulators up to 128, halving above.
+__device__ double np_block(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+  for (int k = 0; k < 8; ++k) r[k] = a[k];
+  int64_t i;
+  for (i = 8; i < n - (n % 8); i += 8)
+    for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[i + k]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+__device__ double np_pairwise(const double* a, int64_t n) {
+  if (n <= 128) return np_block(a, n);
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(np_pairwise(a, n2), np_pairwise(a + n2, n - n2));
+}
+
+__global__ void segment_sum_kernel(const double* __restrict__ row_scores, const int64_t* __restrict__ prog_off,
+                                   int64_t n_prog, double* __restrict__ out) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n_prog) return;
+  int64_t lo = prog_off[p], hi = prog_off[p + 1];
+  out[p] = np_pairwise(row_scores + lo, hi - lo);
+}
+
+}  // namespace lt
+
+using lt::Model;
+using lt::Node;
+
+extern "C" {
+
+// Build a device-resident model from the reference's CostModel.to_json arrays
+// (src/model.py:110-125), trees concatenated; node ids are tree-local.
+int64_t lt_model_create(int n_trees, const int64_t* tree_node_off, const int32_t* feature,
+                        const double* threshold, const int32_t* left, const int32_t* right,
+                        const double* value, const double* eta, double base, int n_features) {
+  if (n_features != lt::NF) { lt::fail("model was built for a different feature layout"); return 0; }
+  std::vector<int> remap(lt::NF, -1);
+  std::vector<int32_t> used;
+  int64_t total = tree_node_off[n_trees];
+  std::vector<Node> nodes((size_t)(total > 0 ? total : 1));
+  std::vector<int32_t> toff(n_trees + 1);
+  for (int t = 0; t < n_trees; ++t) {
+    int64_t o = tree_node_off[t], n = tree_node_off[t + 1] - o;
+    if (n <= 0 || n > 65535) { lt::fail("tree node count out of range"); return 0; }
+    toff[t] = (int32_t)o;
+    for (int64_t i = 0; i < n; ++i) {
+      int32_t f = feature[o + i];
+      Node nd;
+      if (f >= 0) {
+        if (f >= lt::NF) { lt::fail("feature index out of range"); return 0; }
+        if (remap[f] < 0) { remap[f] = (int)used.size(); used.push_back(f); }
+        int32_t l = left[o + i], r = right[o + i];
+        if (l < 0 || l >= n || r < 0 || r >= n) { lt::fail("child index out of range"); return 0; }
+        nd.x = threshold[o + i];
+        nd.feat = remap[f];
+        nd.lr = l | (r << 16);
+      } else {
+        volatile double v = value[o + i];
+        volatile double e = eta[t];
+        nd.x = v * e;                 // IEEE product, same as numpy's value[idx] * eta
+        nd.feat = -1;
+        nd.lr = 0;
+      }
+      nodes[o + i] = nd;
+    }
+  }
+  toff[n_trees] = (int32_t)total;
+  if (used.empty()) used.push_back(0);
+  Model* m = new Model();
+  m->n_trees = n_trees;
+  m->n_used = (int)used.size();
+  m->base = base;
+  if (lt::check_cuda(cudaMalloc(&m->d_nodes, nodes.size() * sizeof(Node)), "cudaMalloc nodes") ||
+      lt::check_cuda(cudaMalloc(&m->d_tree_off, toff.size() * sizeof(int32_t)), "cudaMalloc toff") ||
+      lt::check_cuda(cudaMalloc(&m->d_used, used.size() * sizeof(int32_t)), "cudaMalloc used")) {
+    delete m;
+    return 0;
+  }
+  cudaMemcpy(m->d_nodes, nodes.data(), nodes.size() * sizeof(Node), cudaMemcpyHostToDevice);
+  cudaMemcpy(m->d_tree_off, toff.data(), toff.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  cudaMemcpy(m->d_used, used.data(), used.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (lt::check_cuda(cudaGetLastError(), "model upload")) { delete m; return 0; }
+  return (int64_t)(intptr_t)m;
+}
+
+void lt_model_destroy(int64_t handle) {
+  Model* m = (Model*)(intptr_t)handle;
+  if (!m) return;
+  cudaFree(m->d_nodes);
+  cudaFree(m->d_tree_off);
+  cudaFree(m->d_used);
+  delete m;
+}
+
+int lt_model_info(int64_t handle, int* n_trees, int* n_used_features) {
+  Model* m = (Model*)(intptr_t)handle;
+  if (!m) return lt::fail("null model");
+  *n_trees = m->n_trees;
+  *n_used_features = m->n_used;
+  return 0;
+}
+
+int lt_predict_rows_device(int64_t handle, const double* d_rows, int64_t n_rows, double* d_row_scores,
+                           void* stream) {
+  Model* m = (Model*)(intptr_t)handle;
+  if (!m) return lt::fail("null model");
+  if (n_rows <= 0) return 0;
+  size_t smem = (size_t)lt::ROWS_PER_BLOCK * (m->n_used + 1) * sizeof(double);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    if (lt::check_cuda(cudaFuncSetAttribute(lt::predict_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem), "smem attr"))
+      return -1;
+    configured = smem;
+  }
+  int64_t blocks = (n_rows + lt::ROWS_PER_BLOCK - 1) / lt::ROWS_PER_BLOCK;
+  lt::predict_rows_kernel<<<(unsigned)blocks, lt::ROWS_PER_BLOCK, smem, (cudaStream_t)stream>>>(
+      d_rows, n_rows, m->d_nodes, m->d_tree_off, m->n_trees, m->d_used, m->n_used, m->base, d_row_scores);
+  return lt::check_launch("predict_rows_kernel");
+}
+
+int lt_segment_sum_device(const double* d_row_scores, const int64_t* d_prog_off, int64_t n_prog,
+                          double* d_scores, void* stream) {
+  if (n_prog <= 0) return 0;
+  int64_t blocks = (n_prog + 255) / 256;
+  lt::segment_sum_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_row_scores, d_prog_off, n_prog,
+                                                                             d_scores);
+  return lt::check_launch("segment_sum_kernel");
+}
+
+}  // extern "C"

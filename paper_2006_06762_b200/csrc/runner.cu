@@ -1,0 +1,366 @@
+// Candidate runner: the B200 replacement for the reference's CPU measurement
+// seam (`measure_batch`, src/machine.py:249-285).
+//
+// A candidate is a list of launches of NVRTC-compiled kernels whose only
+// arguments are device buffers ("slots" of a task).  lt_measure():
+//   1. poisons the candidate's output slots with NaN (unwritten cells fail),
+//   2. runs the launch list once (warm-up, also times it),
+//   3. verifies every output against its fp64 ground-truth slot on the device:
+//      max |got - ref| / max(|ref|, 1e-30) (the reference's _check_outputs
+//      metric, src/machine.py:193-208) reduced to one float,
+//   4. re-runs the list r times between CUDA events on the task's stream, r chosen
+//      so the timed region lasts >= min_ms, and reports mean microseconds.
+// Launch failures (e.g. too many registers x threads) are statuses, not errors.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include <math.h>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+#include <mutex>
+#include "common.h"
+
+namespace lt {
+
+// Driver-API entry points resolved through the runtime (cudaGetDriverEntryPoint),
+// so the library loads on hosts without libcuda (the CPU build container).
+struct Drv {
+  CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*ModuleUnload)(CUmodule) = nullptr;
+  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*FuncSetAttribute)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           CUstream, void**, void**) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  bool ok = false;
+};
+static Drv g_drv;
+static std::mutex g_drv_mu;
+
+template <class F>
+static bool resolve(const char* name, F& fn) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
+  fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+static const Drv* drv() {
+  std::lock_guard<std::mutex> g(g_drv_mu);
+  if (!g_drv.ok) {
+    bool ok = resolve("cuModuleLoadData", g_drv.ModuleLoadData) && resolve("cuModuleUnload", g_drv.ModuleUnload) &&
+              resolve("cuModuleGetFunction", g_drv.ModuleGetFunction) &&
+              resolve("cuFuncGetAttribute", g_drv.FuncGetAttribute) &&
+              resolve("cuFuncSetAttribute", g_drv.FuncSetAttribute) &&
+              resolve("cuLaunchKernel", g_drv.LaunchKernel) && resolve("cuGetErrorString", g_drv.GetErrorString);
+    if (!ok) {
+      fail("CUDA driver entry points unavailable (no driver / no device)");
+      return nullptr;
+    }
+    g_drv.ok = true;
+  }
+  return &g_drv;
+}
+
+static const char* cu_str(CUresult r) {
+  const char* s = nullptr;
+  if (g_drv.GetErrorString) g_drv.GetErrorString(r, &s);
+  return s ? s : "unknown CUDA driver error";
+}
+
+static int check_cu(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return 0;
+  return fail(std::string(what) + ": " + cu_str(r));
+}
+
+struct Task {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::unordered_map<int, std::pair<void*, int64_t>> slots;
+  unsigned int* d_err = nullptr;
+};
+
+static std::mutex g_fn_mu;
+static std::unordered_set<CUfunction> g_smem_set;
+
+__global__ void relerr_kernel(const float* __restrict__ got, const double* __restrict__ ref, int64_t n,
+                              unsigned int* __restrict__ out_bits) {
+  float local = 0.0f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double r = ref[i];
+    double g = (double)got[i];
+    double den = fabs(r) > 1e-30 ? fabs(r) : 1e-30;
+    double e = fabs(g - r) / den;
+    float ef = (e <= 3.0e38) ? (float)e : INFINITY;   // NaN and overflow -> inf
+    local = fmaxf(local, ef);
+  }
+  for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+  __shared__ float warp_max[32];
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) warp_max[w] = local;
+  __syncthreads();
+  if (w == 0) {
+    float v = lane < (int)(blockDim.x >> 5) ? warp_max[lane] : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) atomicMax(out_bits, __float_as_uint(v));   // non-negative floats order as uints
+  }
+}
+
+__global__ void fill_u32_kernel(unsigned int* p, int64_t n, unsigned int v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace lt
+
+using lt::Task;
+
+extern "C" {
+
+typedef struct {
+  int64_t func;
+  uint32_t grid[3];
+  uint32_t block[3];
+  uint32_t smem;
+  int32_t n_args;
+  int32_t arg_slot[16];
+} lt_launch;
+
+typedef struct {
+  double cost_us;       // mean device time of the whole launch list
+  double first_us;      // warm-up run
+  float max_rel_err;    // worst over all checked outputs
+  int32_t repeats;
+  int32_t status;       // 0 ok, 1 launch failed (resources), 2 kernel fault
+  char detail[200];
+} lt_measure_record;
+
+int64_t lt_module_load(int device, const void* image, int64_t len) {
+  (void)len;
+  if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return 0;
+  cudaFree(0);  // make the primary context current for the driver API
+  const lt::Drv* d = lt::drv();
+  if (!d) return 0;
+  CUmodule m;
+  if (lt::check_cu(d->ModuleLoadData(&m, image), "cuModuleLoadData")) return 0;
+  return (int64_t)(intptr_t)m;
+}
+
+int lt_module_unload(int64_t module) {
+  const lt::Drv* d = lt::drv();
+  if (!d) return -1;
+  return lt::check_cu(d->ModuleUnload((CUmodule)(intptr_t)module), "cuModuleUnload");
+}
+
+int64_t lt_module_function(int64_t module, const char* name) {
+  const lt::Drv* d = lt::drv();
+  if (!d) return 0;
+  CUfunction f;
+  if (lt::check_cu(d->ModuleGetFunction(&f, (CUmodule)(intptr_t)module, name), "cuModuleGetFunction")) return 0;
+  return (int64_t)(intptr_t)f;
+}
+
+// registers per thread, local (spill+stack) bytes per thread, max threads per block, static smem
+int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads, int* static_smem) {
+  CUfunction f = (CUfunction)(intptr_t)func;
+  const lt::Drv* d = lt::drv();
+  if (!d) return -1;
+  if (lt::check_cu(d->FuncGetAttribute(regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f), "attr") ||
+      lt::check_cu(d->FuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f), "attr") ||
+      lt::check_cu(d->FuncGetAttribute(max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, f), "attr") ||
+      lt::check_cu(d->FuncGetAttribute(static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, f), "attr"))
+    return -1;
+  return 0;
+}
+
+int64_t lt_task_create(int device) {
+  if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return 0;
+  Task* t = new Task();
+  t->device = device;
+  if (lt::check_cuda(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream") ||
+      lt::check_cuda(cudaEventCreate(&t->ev0), "event") || lt::check_cuda(cudaEventCreate(&t->ev1), "event") ||
+      lt::check_cuda(cudaMalloc(&t->d_err, 16), "cudaMalloc")) {
+    delete t;
+    return 0;
+  }
+  return (int64_t)(intptr_t)t;
+}
+
+void lt_task_destroy(int64_t handle) {
+  Task* t = (Task*)(intptr_t)handle;
+  if (!t) return;
+  cudaSetDevice(t->device);
+  cudaStreamSynchronize(t->stream);
+  for (auto& kv : t->slots) cudaFree(kv.second.first);
+  cudaFree(t->d_err);
+  cudaEventDestroy(t->ev0);
+  cudaEventDestroy(t->ev1);
+  cudaStreamDestroy(t->stream);
+  delete t;
+}
+
+void* lt_task_stream(int64_t handle) { return ((Task*)(intptr_t)handle)->stream; }
+
+// (Re)allocate slot `slot` with `bytes` bytes (contents undefined).
+int lt_task_slot(int64_t handle, int slot, int64_t bytes) {
+  Task* t = (Task*)(intptr_t)handle;
+  cudaSetDevice(t->device);
+  auto it = t->slots.find(slot);
+  if (it != t->slots.end()) {
+    if (it->second.second >= bytes) return 0;
+    cudaFree(it->second.first);
+    t->slots.erase(it);
+  }
+  void* p = nullptr;
+  if (lt::check_cuda(cudaMalloc(&p, bytes > 0 ? (size_t)bytes : 16), "cudaMalloc slot")) return -1;
+  t->slots[slot] = {p, bytes};
+  return 0;
+}
+
+int64_t lt_task_slot_ptr(int64_t handle, int slot) {
+  Task* t = (Task*)(intptr_t)handle;
+  auto it = t->slots.find(slot);
+  return it == t->slots.end() ? 0 : (int64_t)(intptr_t)it->second.first;
+}
+
+int lt_task_upload(int64_t handle, int slot, const void* host, int64_t bytes) {
+  Task* t = (Task*)(intptr_t)handle;
+  if (lt_task_slot(handle, slot, bytes)) return -1;
+  cudaSetDevice(t->device);
+  if (lt::check_cuda(cudaMemcpyAsync(t->slots[slot].first, host, (size_t)bytes, cudaMemcpyHostToDevice, t->stream),
+                     "upload"))
+    return -1;
+  return lt::check_cuda(cudaStreamSynchronize(t->stream), "upload sync");
+}
+
+int lt_task_download(int64_t handle, int slot, void* host, int64_t bytes) {
+  Task* t = (Task*)(intptr_t)handle;
+  auto it = t->slots.find(slot);
+  if (it == t->slots.end() || it->second.second < bytes) return lt::fail("download: bad slot");
+  cudaSetDevice(t->device);
+  if (lt::check_cuda(cudaMemcpyAsync(host, it->second.first, (size_t)bytes, cudaMemcpyDeviceToHost, t->stream),
+                     "download"))
+    return -1;
+  return lt::check_cuda(cudaStreamSynchronize(t->stream), "download sync");
+}
+
+static int launch_list(Task* t, const lt_launch* ls, int n, std::string& why) {
+  const lt::Drv* d = lt::drv();
+  if (!d) { why = "CUDA driver unavailable"; return 2; }
+  for (int i = 0; i < n; ++i) {
+    const lt_launch& L = ls[i];
+    CUfunction f = (CUfunction)(intptr_t)L.func;
+    void* ptrs[16];
+    void* args[16];
+    if (L.n_args > 16) { why = "too many kernel arguments"; return 1; }
+    for (int a = 0; a < L.n_args; ++a) {
+      auto it = t->slots.find(L.arg_slot[a]);
+      if (it == t->slots.end()) { why = "launch references an unallocated slot"; return 1; }
+      ptrs[a] = it->second.first;
+      args[a] = &ptrs[a];
+    }
+    if (L.smem > 48 * 1024) {
+      std::lock_guard<std::mutex> g(lt::g_fn_mu);
+      if (!lt::g_smem_set.count(f)) {
+        CUresult r = d->FuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)L.smem);
+        if (r != CUDA_SUCCESS) {
+          why = std::string("dynamic shared memory not granted: ") + lt::cu_str(r);
+          return 1;
+        }
+        lt::g_smem_set.insert(f);
+      }
+    }
+    CUresult r = d->LaunchKernel(f, L.grid[0], L.grid[1], L.grid[2], L.block[0], L.block[1], L.block[2], L.smem,
+                                 (CUstream)t->stream, args, nullptr);
+    if (r != CUDA_SUCCESS) {
+      why = std::string("launch failed: ") + lt::cu_str(r);
+      return r == CUDA_ERROR_LAUNCH_OUT_OF_RESOURCES || r == CUDA_ERROR_INVALID_VALUE ? 1 : 2;
+    }
+  }
+  return 0;
+}
+
+// Run a launch list once, synchronously (ground truth, packing, warm-ups).
+int lt_task_run(int64_t handle, const lt_launch* launches, int n) {
+  Task* t = (Task*)(intptr_t)handle;
+  cudaSetDevice(t->device);
+  std::string why;
+  if (launch_list(t, launches, n, why)) return lt::fail(why);
+  return lt::check_cuda(cudaStreamSynchronize(t->stream), "run");
+}
+
+int lt_measure(int64_t handle, const lt_launch* launches, int n_launch, const int32_t* check_pairs,
+               const int64_t* numel, int n_check, int min_repeat, int max_repeat, double min_ms,
+               lt_measure_record* rec) {
+  Task* t = (Task*)(intptr_t)handle;
+  memset(rec, 0, sizeof *rec);
+  cudaSetDevice(t->device);
+  std::string why;
+  // 1. poison outputs
+  for (int c = 0; c < n_check; ++c) {
+    auto it = t->slots.find(check_pairs[2 * c]);
+    if (it == t->slots.end()) return lt::fail("measure: output slot missing");
+    lt::fill_u32_kernel<<<256, 256, 0, t->stream>>>((unsigned int*)it->second.first, numel[c], 0x7fc00000u);
+  }
+  // 2. warm-up (timed)
+  cudaEventRecord(t->ev0, t->stream);
+  int st = launch_list(t, launches, n_launch, why);
+  if (st) {
+    rec->status = st;
+    snprintf(rec->detail, sizeof rec->detail, "%s", why.c_str());
+    cudaStreamSynchronize(t->stream);
+    cudaGetLastError();
+    return 0;
+  }
+  cudaEventRecord(t->ev1, t->stream);
+  cudaError_t e = cudaStreamSynchronize(t->stream);
+  if (e != cudaSuccess) {
+    rec->status = 2;
+    snprintf(rec->detail, sizeof rec->detail, "kernel fault: %s", cudaGetErrorString(e));
+    return lt::fail(std::string("kernel fault (context is unusable): ") + cudaGetErrorString(e));
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t->ev0, t->ev1);
+  rec->first_us = ms * 1000.0;
+  // 3. verify against the fp64 ground truth
+  cudaMemsetAsync(t->d_err, 0, 4, t->stream);
+  for (int c = 0; c < n_check; ++c) {
+    const float* got = (const float*)t->slots[check_pairs[2 * c]].first;
+    auto it = t->slots.find(check_pairs[2 * c + 1]);
+    if (it == t->slots.end()) return lt::fail("measure: reference slot missing");
+    int64_t n = numel[c];
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 1184) blocks = 1184;
+    if (blocks < 1) blocks = 1;
+    lt::relerr_kernel<<<blocks, 256, 0, t->stream>>>(got, (const double*)it->second.first, n, t->d_err);
+  }
+  unsigned int bits = 0;
+  cudaMemcpyAsync(&bits, t->d_err, 4, cudaMemcpyDeviceToHost, t->stream);
+  if (lt::check_cuda(cudaStreamSynchronize(t->stream), "verify")) return -1;
+  float err;
+  memcpy(&err, &bits, 4);
+  rec->max_rel_err = err;
+  // 4. timed repeats
+  double first_ms = ms > 1e-4 ? ms : 1e-4;
+  int r = (int)ceil(min_ms / first_ms);
+  if (r < min_repeat) r = min_repeat;
+  if (r > max_repeat) r = max_repeat;
+  cudaEventRecord(t->ev0, t->stream);
+  for (int k = 0; k < r; ++k)
+    if (launch_list(t, launches, n_launch, why)) return lt::fail(why);
+  cudaEventRecord(t->ev1, t->stream);
+  if (lt::check_cuda(cudaStreamSynchronize(t->stream), "timed runs")) return -1;
+  cudaEventElapsedTime(&ms, t->ev0, t->ev1);
+  rec->repeats = r;
+  rec->cost_us = ms * 1000.0 / r;
+  return 0;
+}
+
+}  // extern "C"

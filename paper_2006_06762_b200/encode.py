@@ -1,0 +1,198 @@
+"""State encoder: Program objects -> flat int32 statement records for the
+batched feature kernel (`csrc/features.cu`).
+
+Everything the reference's `analyze_program` (`src/features.py:161-284`)
+derives *structurally* is resolved here, once, on the host; everything it
+derives *arithmetically* (decode-AST intervals and evaluations, hulls, reuse,
+strides, working sets, the 164-wide row) is left to the GPU.  Host-side
+resolutions, each cited:
+
+* live statements in stage order, nest = attach-chain host loops + own loops
+  with extent > 1 (`_nest_above`, `src/features.py:114-121,163-170`);
+* loop identity is *by id string* (`src/features.py:224-225`): each nest
+  position carries the index of the own loop with the same id (or -1), and each
+  own loop carries the last nest position with its id (the `free` test of
+  `ws_inside`, `src/features.py:266-274`);
+* buffer views in first-access order, reads pre-order then the write
+  (`src/features.py:183-200`); a view's dims come from its first access;
+  packed constants add (stride, extent) per physical dim (`_phys_decodes`,
+  `src/features.py:124-140`);
+* buffer-name rank for the (-bytes, name) ordering (`src/features.py:398`);
+* op counts of the stage expression (`src/expr.py:303-327`).
+
+Record layout (int32 words, one record per statement, see include/loomtune_b200.h):
+
+  header[HDR]  n_nest own_start n_loops n_iter n_views unroll n_live has_reduce
+               ops[9]  n_nodes
+  nest[n_nest]  x (extent, kind, annotation, own_index)
+  loops[n_loops] x (extent, kind, last_nest_pos)
+  iter[n_iter]  x (node_offset, node_count)          postfix decode ASTs per iterator
+  nodes[n_nodes] x (op, arg)                          op: 0 var(own loop idx) 1 const
+                                                         2 add 3 mul(c) 4 div(c) 5 mod(c)
+  views[n_views]: n_marks has_write name_rank n_dims,
+                  dims: (size, pack_stride, pack_ext, const, n_terms, (iter, coeff) x n_terms)
+                  pack_ext == 0 means "not packed".
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .state.expr import kind, op_counts, reads
+
+HDR = 18
+OP_VAR, OP_CONST, OP_ADD, OP_MUL, OP_DIV, OP_MOD = range(6)
+ANN = {None: 0, "parallel": 1, "vectorize": 2}
+KINDS = ("add", "sub", "mul", "div", "minmax", "cmp", "math_call", "select", "other")
+
+
+class EncodeError(ValueError):
+    pass
+
+
+def _ops(expr, cache: dict) -> list:
+    key = id(expr)
+    hit = cache.get(key)
+    if hit is None or hit[0] is not expr:
+        c = op_counts(expr) if expr is not None else {}
+        hit = (expr, [c.get(k, 0) for k in KINDS])
+        cache[key] = hit
+    return hit[1]
+
+
+def _postfix(d, loop_idx: dict, out: list) -> None:
+    k = kind(d)
+    if k == "DVar":
+        if d.loop not in loop_idx:
+            raise EncodeError(f"decode references unknown loop {d.loop!r}")
+        out += (OP_VAR, loop_idx[d.loop])
+    elif k == "DConst":
+        out += (OP_CONST, int(d.value))
+    elif k == "DAdd":
+        _postfix(d.a, loop_idx, out)
+        _postfix(d.b, loop_idx, out)
+        out += (OP_ADD, 0)
+    else:
+        if d.c is None:
+            raise EncodeError("symbolic factor in decode")
+        _postfix(d.a, loop_idx, out)
+        out += ({"DMul": OP_MUL, "DDiv": OP_DIV, "DMod": OP_MOD}[k], int(d.c))
+
+
+def _stage_map(p) -> dict:
+    return {s.name: s for s in p.stages}
+
+
+def _nest_above(smap: dict, s) -> list:
+    if s.compute_at is None:
+        return []
+    tname, lid = s.compute_at
+    t = smap[tname]
+    ids = [l.id for l in t.loops]
+    return _nest_above(smap, t) + list(t.loops[: ids.index(lid) + 1])
+
+
+def encode_program(p, out: list, ops_cache: dict) -> int:
+    """Append one record per live statement of `p` to `out` (a list of int
+    lists); returns the number of statements."""
+    smap = _stage_map(p)
+    layouts = dict(p.layouts)
+    live = [s for s in p.stages if not s.inlined]
+    shapes = {s.name: tuple(e for _, e in s.space) for s in p.stages}
+    for s in live:
+        above = [l for l in _nest_above(smap, s) if (l.extent or 1) > 1]
+        own = [l for l in s.loops if (l.extent or 1) > 1]
+        nest = above + own
+        loop_idx = {l.id: j for j, l in enumerate(s.loops)}
+        last_pos = {}
+        for q, l in enumerate(nest):
+            last_pos[l.id] = q
+        iters = [n for n, _ in s.index_map]
+        iter_idx = {n: j for j, n in enumerate(iters)}
+        dmap = dict(s.index_map)
+
+        nodes: list = []
+        iter_tab: list = []
+        extra_iters: list = []          # iterators read but absent from the map -> DVar(name)
+        for n in iters:
+            start = len(nodes) // 2
+            _postfix(dmap[n], loop_idx, nodes)
+            iter_tab += (start, len(nodes) // 2 - start)
+
+        def iter_slot(name: str) -> int:
+            if name in iter_idx:
+                return iter_idx[name]
+            if name not in loop_idx:
+                raise EncodeError(f"iterator {name!r} has no decode and no loop")
+            iter_idx[name] = len(iters) + len(extra_iters)
+            extra_iters.append(name)
+            start = len(nodes) // 2
+            nodes.extend((OP_VAR, loop_idx[name]))
+            iter_tab.extend((start, 1))
+            return iter_idx[name]
+
+        views: dict = {}
+        order: list = []
+        accesses = [(r.buffer, r.index, 0) for r in reads(s.expr)] if s.expr is not None else []
+        accesses.append((s.name, None, 1))
+        for buf, idx, is_w in accesses:
+            if buf not in views:
+                if idx is None:
+                    lins = [((n, 1),) for n, _ in s.space]
+                    consts = [0] * len(s.space)
+                else:
+                    lins = [l.terms for l in idx]
+                    consts = [l.const for l in idx]
+                dims = []
+                desc = layouts.get(buf)
+                logical = [(consts[d], [(iter_slot(n), c) for n, c in lins[d]]) for d in range(len(lins))]
+                if desc is not None:
+                    for i, (d, ext) in enumerate(desc):
+                        st = 1
+                        for d2, e2 in desc[i + 1:]:
+                            if d2 == d:
+                                st *= e2
+                        dims.append((ext, st, ext, logical[d]))
+                else:
+                    shape = shapes[buf] if buf in shapes else p.dag.node(buf).shape
+                    dims = [(shape[d], 1, 0, logical[d]) for d in range(len(logical))]
+                views[buf] = [0, 0, dims]
+                order.append(buf)
+            views[buf][0] += 1
+            views[buf][1] |= is_w
+        rank = {b: r for r, b in enumerate(sorted(order))}
+
+        rec = [len(nest), len(above), len(s.loops), len(iter_tab) // 2, len(order),
+               int(s.pragma_unroll), len(live), 1 if s.reduce else 0]
+        rec += _ops(s.expr, ops_cache)
+        rec.append(len(nodes) // 2)
+        for l in nest:
+            rec += (int(l.extent), 0 if l.kind == "space" else 1, ANN.get(l.annotation, 0),
+                    loop_idx.get(l.id, -1))
+        for l in s.loops:
+            rec += (int(l.extent or 1), 0 if l.kind == "space" else 1, last_pos.get(l.id, -1))
+        rec += iter_tab
+        rec += nodes
+        for b in order:
+            n_marks, has_w, dims = views[b]
+            rec += (n_marks, has_w, rank[b], len(dims))
+            for size, st, pext, (const, terms) in dims:
+                rec += (int(size), st, pext, int(const), len(terms))
+                for it, c in terms:
+                    rec += (it, int(c))
+        out.append(rec)
+    return len(live)
+
+
+def encode_batch(programs) -> tuple:
+    """-> (words int32[], stmt_offsets int64[n_stmt+1], prog_row_offsets int64[n_prog+1])."""
+    recs: list = []
+    prog_off = [0]
+    cache: dict = {}
+    for p in programs:
+        prog_off.append(prog_off[-1] + encode_program(p, recs, cache))
+    lens = np.fromiter((len(r) for r in recs), dtype=np.int64, count=len(recs))
+    stmt_off = np.zeros(len(recs) + 1, dtype=np.int64)
+    np.cumsum(lens, out=stmt_off[1:])
+    words = np.fromiter((w for r in recs for w in r), dtype=np.int32, count=int(stmt_off[-1]))
+    return words, stmt_off, np.asarray(prog_off, dtype=np.int64)

@@ -1,0 +1,365 @@
+"""GPU measurement: drop-in for the reference's `measure_batch`
+(`src/machine.py:249-285`) with the same signature, result type and status
+semantics.
+
+Per candidate: `validate` (host, reference messages) -> lower to CUDA
+(`lower.py`) -> compile with exact constants in the multi-process NVRTC pool
+(cached on disk) -> run on the B200, verify every output against an fp64
+ground truth on the device (max relative error <= `GPU_TOL`, the north star's
+1e-4 for fp32) -> time with CUDA events.  `cost` is device microseconds.
+
+Statuses: INVALID (validation failure, no legal launch, compile/launch
+failure, or wrong output — detail says which), TIMEOUT (cost >=
+`limits.cost_ceiling`, read in microseconds), VALID.  Throughput is
+`min(valid costs, best_cost) / cost` exactly as the reference normalises
+(`src/machine.py:276-285`).  `spec` (the CPU machine model) is accepted and
+ignored.  Inputs are `random_inputs(dag, default_rng(limits.check_seed))`
+(`src/interp.py:38-43`), generated once per DAG and kept resident in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+import math
+import os
+import time
+from collections import OrderedDict
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from . import runtime as rt
+from .lower import Lowered, LoweringError, lower, reference_lowering
+from .state.ir import validate
+
+VALID, INVALID, TIMEOUT = "valid", "invalid", "timeout"
+GPU_TOL = 1e-4
+NVRTC_OPTS = "--gpu-architecture=sm_100a\n-default-device\n-lineinfo"
+
+
+@dataclass(frozen=True)
+class MeasureResult:
+    """Same fields as `src/machine.py:51-56`."""
+    cost: float
+    throughput: float
+    status: str
+    detail: str = ""
+
+
+@dataclass(frozen=True)
+class MeasureLimits:
+    """Same fields as `src/machine.py:241-246`; cost_ceiling is in microseconds here."""
+    cost_ceiling: float | None = None
+    check_cap: int = 8
+    check_tol: float = 1e-5
+    check_seed: int = 0
+
+
+@dataclass
+class Record:
+    """Per-candidate telemetry (logged beside MeasureResult)."""
+    status: str = INVALID
+    detail: str = ""
+    cost_us: float = math.inf
+    first_us: float = 0.0
+    max_rel_err: float = math.nan
+    repeats: int = 0
+    compile_s: float = 0.0
+    cache_hit: bool = False
+    lower_s: float = 0.0
+    info: dict = field(default_factory=dict)
+
+
+def random_inputs(dag, seed: int) -> dict:
+    """`random_inputs` (`src/interp.py:38-43`): U(0.25, 1) per placeholder in node order."""
+    rng = np.random.default_rng(seed)
+    return {n.name: rng.uniform(0.25, 1.0, size=n.shape) for n in dag.nodes if n.is_placeholder}
+
+
+def pack(arr: np.ndarray, desc) -> np.ndarray:
+    """Physical layout of a packed constant (LayoutRewrite, `src/ir.py:747-760`):
+    one physical dim per descriptor entry, outer to inner."""
+    phys_shape = tuple(e for _, e in desc)
+    grids = np.indices(phys_shape)
+    idx = [np.zeros(phys_shape, dtype=np.int64) for _ in range(arr.ndim)]
+    for j, (d, e) in enumerate(desc):
+        st = 1
+        for d2, e2 in desc[j + 1:]:
+            if d2 == d:
+                st *= e2
+        idx[d] = idx[d] + grids[j] * st
+    return arr[tuple(idx)]
+
+
+def _dag_key(dag, seed: int) -> str:
+    return hashlib.sha1((json.dumps(dag.to_json(), sort_keys=True) + f"#{seed}").encode()).hexdigest()
+
+
+class _DagContext:
+    """Device-resident state for one DAG: inputs (fp32 + fp64), fp64 ground truth,
+    packed constants, candidate scratch buffers."""
+
+    def __init__(self, runner: "Runner", dag, seed: int):
+        self.r = runner
+        self.dag = dag
+        lib = runner.lib
+        self.task = lib.lt_task_create(runner.device)
+        if not self.task:
+            raise rt.NativeError(lib.lt_last_error().decode())
+        self.slots: dict = {}
+        self.sizes: dict = {}
+        self.inputs = random_inputs(dag, seed)
+        self.h2d_bytes = 0
+        for name, arr in self.inputs.items():
+            self._upload(f"in:{name}", np.ascontiguousarray(arr, dtype=np.float32))
+            self._upload(f"in64:{name}", np.ascontiguousarray(arr, dtype=np.float64))
+        # fp64 ground truth, computed once on the device from the fp64 inputs
+        ref = reference_lowering(dag)
+        funcs = runner.compile_and_load([ref.source], [[k.entry for k in ref.kernels]])[0]
+        if isinstance(funcs, str):
+            raise rt.NativeError(f"ground-truth kernel failed to compile: {funcs}")
+        for name, b in ref.buffers.items():
+            if b.role in ("temp", "output"):
+                self.slot(f"ref:{name}", b.numel * 8)
+        launches = self._launches(ref, funcs, fp64=True)
+        rt.check(lib.lt_task_run(self.task, ctypes.addressof(launches), len(ref.kernels)), "ground truth")
+        self.outputs = list(ref.outputs)
+
+    def slot(self, key: str, nbytes: int) -> int:
+        if key not in self.slots:
+            self.slots[key] = len(self.slots)
+        if self.sizes.get(key, -1) < nbytes:
+            rt.check(self.r.lib.lt_task_slot(self.task, self.slots[key], nbytes), f"alloc {key}")
+            self.sizes[key] = nbytes
+        return self.slots[key]
+
+    def _upload(self, key: str, arr: np.ndarray) -> int:
+        sid = self.slot(key, arr.nbytes)
+        rt.check(self.r.lib.lt_task_upload(self.task, sid, arr.ctypes.data, arr.nbytes), f"upload {key}")
+        self.h2d_bytes += arr.nbytes
+        return sid
+
+    def buffer_slot(self, b, fp64: bool) -> int:
+        if b.role == "input":
+            return self.slots[f"in64:{b.name}" if fp64 else f"in:{b.name}"]
+        if b.role == "packed":
+            key = f"pk:{b.source}:{b.desc}"
+            if key not in self.slots:
+                self._upload(key, np.ascontiguousarray(pack(self.inputs[b.source], b.desc), dtype=np.float32))
+            return self.slots[key]
+        if fp64:
+            return self.slots[f"ref:{b.name}"]
+        return self.slot(f"buf:{b.name}", b.numel * 4)
+
+    def _launches(self, lo: Lowered, funcs: list, fp64: bool = False):
+        arr = (rt.Launch * len(lo.kernels))()
+        for i, (k, fn) in enumerate(zip(lo.kernels, funcs)):
+            L = arr[i]
+            L.func = fn
+            L.grid[:] = (k.grid, 1, 1)
+            L.block[:] = (k.block, 1, 1)
+            L.smem = k.smem
+            L.n_args = len(k.args)
+            for a, name in enumerate(k.args):
+                L.arg_slot[a] = self.buffer_slot(lo.buffers[name], fp64)
+        return arr
+
+    def measure(self, lo: Lowered, funcs: list, min_ms: float, max_repeat: int) -> rt.MeasureRecord:
+        launches = self._launches(lo, funcs)
+        pairs, numel = [], []
+        for name in lo.outputs:
+            b = lo.buffers[name]
+            pairs += [self.buffer_slot(b, False), self.slots[f"ref:{name}"]]
+            numel.append(b.numel)
+        pairs_a = np.asarray(pairs, np.int32)
+        numel_a = np.asarray(numel, np.int64)
+        rec = rt.MeasureRecord()
+        rt.check(self.r.lib.lt_measure(self.task, ctypes.addressof(launches), len(lo.kernels),
+                                       rt.ptr(pairs_a, rt.c_i32p), rt.ptr(numel_a, rt.c_i64p), len(numel),
+                                       2, max_repeat, min_ms, ctypes.addressof(rec)), "lt_measure")
+        return rec
+
+    def download(self, name: str, numel: int, fp64: bool = False) -> np.ndarray:
+        out = np.empty(numel, np.float64 if fp64 else np.float32)
+        key = f"ref:{name}" if fp64 else f"buf:{name}"
+        rt.check(self.r.lib.lt_task_download(self.task, self.slots[key], out.ctypes.data, out.nbytes), "download")
+        return out
+
+
+class Runner:
+    """Per-process GPU runner: one device, one compile pool, DAG contexts, module cache."""
+
+    def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
+                 min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0):
+        self.lib = rt.load()
+        self.device = device
+        rt.check(self.lib.lt_set_device(device), "set device")
+        self.workers = workers or max(1, (os.cpu_count() or 2) - 1)
+        self.cache_dir = cache_dir if cache_dir is not None else os.environ.get(
+            "LT_CUBIN_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "loomtune_b200", "cubin"))
+        rt.check(self.lib.lt_pool_start(self.workers, self.cache_dir.encode() if self.cache_dir else None,
+                                        compile_timeout), "compile pool")
+        self.min_ms, self.max_repeat = min_ms, max_repeat
+        self.ctx: dict = {}
+        self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
+        self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0}
+
+    def close(self):
+        for m, _ in self.modules.values():
+            self.lib.lt_module_unload(m)
+        self.modules.clear()
+        for c in self.ctx.values():
+            self.lib.lt_task_destroy(c.task)
+        self.ctx.clear()
+        self.lib.lt_pool_stop()
+
+    def context(self, dag, seed: int) -> _DagContext:
+        key = _dag_key(dag, seed)
+        if key not in self.ctx:
+            self.ctx[key] = _DagContext(self, dag, seed)
+        return self.ctx[key]
+
+    # -- compile + load ------------------------------------------------------
+    def submit(self, source: str) -> int:
+        b = source.encode()
+        return self.lib.lt_compile_submit(b, len(b), NVRTC_OPTS.encode())
+
+    def collect(self, job: int):
+        st, secs, hit, n = ctypes.c_int(), ctypes.c_double(), ctypes.c_int(), ctypes.c_int64()
+        rt.check(self.lib.lt_compile_wait(job, ctypes.byref(st), ctypes.byref(secs), ctypes.byref(hit),
+                                          ctypes.byref(n)), "compile wait")
+        buf = ctypes.create_string_buffer(max(1, n.value))
+        rt.check(self.lib.lt_compile_fetch(job, buf, n.value), "compile fetch")
+        return st.value, secs.value, bool(hit.value), buf.raw[:n.value]
+
+    def load(self, key: str, image: bytes, entries: list) -> list:
+        if key in self.modules:
+            self.modules.move_to_end(key)
+            return self.modules[key][1]
+        m = self.lib.lt_module_load(self.device, image, len(image))
+        if not m:
+            raise rt.NativeError(f"module load: {self.lib.lt_last_error().decode()}")
+        funcs = []
+        for e in entries:
+            f = self.lib.lt_module_function(m, e.encode())
+            if not f:
+                raise rt.NativeError(f"function {e}: {self.lib.lt_last_error().decode()}")
+            funcs.append(f)
+        self.modules[key] = (m, funcs)
+        while len(self.modules) > 512:
+            _, (old, _) = self.modules.popitem(last=False)
+            self.lib.lt_module_unload(old)
+        return funcs
+
+    def compile_and_load(self, sources: list, entries: list) -> list:
+        jobs = [self.submit(s) for s in sources]
+        out = []
+        for s, j, e in zip(sources, jobs, entries):
+            st, secs, hit, data = self.collect(j)
+            if st != 0:
+                out.append(data.decode(errors="replace"))
+            else:
+                out.append(self.load(hashlib.sha1(s.encode()).hexdigest(), data, e))
+        return out
+
+    # -- measurement ---------------------------------------------------------
+    def measure_programs(self, programs: list, seed: int = 0) -> list:
+        recs = [Record() for _ in programs]
+        pending = []
+        for i, p in enumerate(programs):
+            bad = validate(p)
+            if bad:
+                recs[i].detail = bad[0]
+                continue
+            t0 = time.perf_counter()
+            try:
+                lo = lower(p)
+            except LoweringError as e:
+                recs[i].detail = f"gpu: {e}"
+                recs[i].lower_s = time.perf_counter() - t0
+                continue
+            recs[i].lower_s = time.perf_counter() - t0
+            recs[i].info = lo.info
+            key = hashlib.sha1(lo.source.encode()).hexdigest()
+            job = None if key in self.modules else self.submit(lo.source)
+            pending.append((i, p, lo, key, job))
+        for i, p, lo, key, job in pending:
+            rec = recs[i]
+            if job is None:
+                funcs = self.load(key, b"", [k.entry for k in lo.kernels])
+                rec.cache_hit = True
+            else:
+                st, secs, hit, data = self.collect(job)
+                rec.compile_s, rec.cache_hit = secs, hit
+                self.stats["compile_s"] += secs
+                self.stats["cache_hits" if hit else "compiled"] += 1
+                if st != 0:
+                    rec.detail = "gpu: compile failed: " + data.decode(errors="replace").strip()[:300]
+                    continue
+                funcs = self.load(key, data, [k.entry for k in lo.kernels])
+            ctx = self.context(p.dag, seed)
+            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat)
+            self.stats["measured"] += 1
+            rec.first_us, rec.repeats = m.first_us, m.repeats
+            rec.max_rel_err = float(m.max_rel_err)
+            if m.status != 0:
+                rec.detail = "gpu: " + m.detail.decode(errors="replace")
+                continue
+            if not (rec.max_rel_err <= GPU_TOL):
+                names = ",".join(lo.outputs)
+                rec.detail = f"output {names} differs from reference (max rel err {rec.max_rel_err:.3g})"
+                continue
+            rec.status = VALID
+            rec.cost_us = m.cost_us
+        return recs
+
+
+_RUNNER: Runner | None = None
+
+
+def get_runner(**kw) -> Runner:
+    global _RUNNER
+    if _RUNNER is None:
+        _RUNNER = Runner(**kw)
+    return _RUNNER
+
+
+def configure(**kw) -> Runner:
+    """(Re)create the process-wide runner (device, workers, cache_dir, min_ms...)."""
+    global _RUNNER
+    if _RUNNER is not None:
+        _RUNNER.close()
+    _RUNNER = Runner(**kw)
+    return _RUNNER
+
+
+def normalise(recs: list, best_cost=None, cost_ceiling=None) -> list:
+    """Records -> MeasureResults with the reference's statuses and normalisation."""
+    results, costs = [], []
+    for r in recs:
+        if r.status != VALID:
+            results.append(MeasureResult(math.inf, 0.0, INVALID, r.detail))
+            costs.append(None)
+        elif cost_ceiling is not None and r.cost_us >= cost_ceiling:
+            results.append(MeasureResult(r.cost_us, 0.0, TIMEOUT))
+            costs.append(None)
+        else:
+            results.append(MeasureResult(r.cost_us, 0.0, VALID))
+            costs.append(r.cost_us)
+    valid = [c for c in costs if c is not None]
+    if best_cost is not None:
+        valid.append(best_cost)
+    if not valid:
+        return results
+    best = min(valid)
+    return [replace(r, throughput=best / c) if c is not None else r for r, c in zip(results, costs)]
+
+
+def measure_batch(programs, spec=None, limits=None, best_cost=None) -> list:
+    """Drop-in for `loomtune.machine.measure_batch` (`src/machine.py:249-285`)."""
+    limits = limits if limits is not None else MeasureLimits()
+    runner = get_runner()
+    recs = runner.measure_programs(list(programs), seed=getattr(limits, "check_seed", 0))
+    return normalise(recs, best_cost, getattr(limits, "cost_ceiling", None))

@@ -1,0 +1,66 @@
+"""GPU feature kernel and tree kernel vs the reference's own outputs (golden) and the oracle."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-6   # north star: features within 1e-6 (absolute on the log2-compressed row)
+
+
+def test_features_match_reference_golden(corpus):
+    from paper_2006_06762_b200.features import extract_features_batch
+    got = extract_features_batch(corpus.programs)
+    worst, exact = 0.0, 0
+    for i, g in enumerate(got):
+        w = corpus.features_of(i)
+        assert g.shape == w.shape, i
+        assert np.isfinite(g).all(), i
+        d = float(np.max(np.abs(g - w))) if g.size else 0.0
+        worst = max(worst, d)
+        exact += bool(np.array_equal(g, w))
+    assert worst <= TOL, worst
+    print(f"features: {exact}/{len(got)} programs bit-exact, worst abs diff {worst:.3g}")
+
+
+def test_scores_match_reference_golden(corpus):
+    from paper_2006_06762_b200.model import GpuCostModel
+    m = GpuCostModel.from_json(corpus.model_json)
+    got = m.predict_batch(corpus.programs)
+    want = corpus.scores
+    rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-12)
+    assert float(rel.max()) <= 1e-5, float(rel.max())
+    print(f"scores: {int((got == want).sum())}/{len(got)} bit-exact")
+
+
+def test_predict_rows_matches_oracle_on_golden_rows(corpus):
+    from oracle import predict as OP
+    from paper_2006_06762_b200.model import GpuCostModel
+    m = GpuCostModel.from_json(corpus.model_json)
+    X = corpus.rows
+    got = m.predict_rows(X)
+    want = OP.predict_rows(OP.load_model(corpus.model_json), X)
+    assert np.array_equal(got, want)
+
+
+def test_empty_model_scores_zero(corpus):
+    from paper_2006_06762_b200.model import GpuCostModel
+    assert (GpuCostModel().predict_batch(corpus.programs[:10]) == 0.0).all()
+
+
+def test_pairwise_sum_order_many_rows():
+    """Programs with >= 8 rows must follow numpy's pairwise summation."""
+    from paper_2006_06762_b200.model import GpuCostModel
+    rng = np.random.default_rng(0)
+    model = GpuCostModel.from_json({"base": 0.0, "n_features": 164, "shrinkage": 0.3, "depth": 1, "trees": [
+        {"eta": 1.0, "feature": [0, -1, -1], "threshold": [0.5, 0.0, 0.0], "left": [1, 0, 0], "right": [2, 0, 0],
+         "value": [0.0, 1e16, 1.0]}]})
+    mats = []
+    for n in (1, 3, 7, 8, 11, 127, 129, 300):
+        X = rng.random((n, 164))
+        X[0, 0] = 0.1  # first row -> 1e16 leaf, the rest mostly 1.0 or 1e16
+        mats.append(X)
+    got = model.predict_matrices(mats)
+    for g, X in zip(got, mats):
+        rows = np.where(X[:, 0] <= 0.5, 1e16, 1.0)
+        assert g == float(rows.sum())

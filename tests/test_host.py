@@ -1,0 +1,142 @@
+"""CPU-only checks: State mirror, encoder, lowering/codegen, native library surface."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2006_06762_b200 import encode, lower
+from paper_2006_06762_b200.state import build, history_to_json, naive_program, validate
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_SRC = "/root/reference/pkg/src"
+
+
+def test_corpus_replays_and_validates(corpus):
+    # every golden State replays in the mirror and round-trips its history JSON
+    for p, e in zip(corpus.programs, corpus.entries):
+        assert history_to_json(p.history) == e["history"]
+        assert validate(p) == []
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference not present (GPU box)")
+def test_mirror_replay_structure_equals_reference(corpus):
+    import sys
+    sys.path.insert(0, REF_SRC)
+    import loomtune as LT
+    from loomtune.ir import history_from_json as r_h
+    for p, e in list(zip(corpus.programs, corpus.entries))[::5]:
+        rdag = LT.ComputeDAG.from_json(corpus.dags[e["dag"]].to_json())
+        q = LT.replay(rdag, r_h(e["history"]))
+        assert [s.name for s in p.stages] == [s.name for s in q.stages]
+        for a, b in zip(p.stages, q.stages):
+            assert [(l.id, l.extent, l.kind, l.annotation, l.lin_stride) for l in a.loops] == \
+                   [(l.id, l.extent, l.kind, l.annotation, l.lin_stride) for l in b.loops]
+            assert repr(a.index_map) == repr(b.index_map)
+            assert (a.compute_at, a.pragma_unroll, a.inlined) == (b.compute_at, b.pragma_unroll, b.inlined)
+        assert tuple(p.layouts) == tuple(q.layouts)
+
+
+def test_encoder_records(corpus):
+    words, stmt_off, prog_off = encode.encode_batch(corpus.programs)
+    assert stmt_off[-1] == len(words)
+    assert prog_off[-1] == len(stmt_off) - 1 == len(corpus.rows)
+    for i in range(len(corpus.programs)):
+        assert prog_off[i + 1] - prog_off[i] == corpus.offsets[i + 1] - corpus.offsets[i]
+    # header sanity: n_nest, own_start, n_views within kernel limits
+    for s in range(len(stmt_off) - 1):
+        r = words[stmt_off[s]:stmt_off[s + 1]]
+        assert 0 <= r[1] <= r[0] <= 32 and r[2] <= 64 and r[3] <= 24 and 1 <= r[4] <= 12
+
+
+def test_lowering_covers_corpus(corpus):
+    ok = illegal = 0
+    for p in corpus.programs:
+        try:
+            lo = lower.lower(p)
+        except lower.LoweringError as e:
+            assert re.search(r"threads|shared memory|accumulators|virtual threads|unrolled", str(e)), str(e)
+            illegal += 1
+            continue
+        ok += 1
+        assert lo.kernels and all(k.block <= 1024 and k.smem <= lower.MAX_SMEM for k in lo.kernels)
+        assert set(lo.outputs) == set(p.dag.outputs)
+    assert ok > 0.8 * len(corpus.programs), (ok, illegal)
+
+
+def test_identical_kernels_for_cpu_only_differences():
+    """Fusing the parallel band differently (a CPU decision) must not change the GPU kernel."""
+    from paper_2006_06762_b200.state import Annotate, Fuse, Split, Reorder, apply_step, SetPragma
+    dag = build("matmul", n=64, m=64, k=64)
+    p = naive_program(dag)
+    for st in (Split("C", "i", (2, 4, 2, 1)), Split("C", "j", (2, 4, 2, 2)), Split("C", "k", (4, 4)),
+               Reorder("C", ("i.0", "j.0", "i.1", "j.1", "i.2", "j.2", "k.0", "k.1", "i.3", "j.3", "k.2",
+                             "i.4", "j.4")), SetPragma("C", 512)):
+        p = apply_step(p, st)
+    a = apply_step(apply_step(p, Fuse("C", "i.0", "j.0")), Annotate("C", "i.0@j.0", "parallel"))
+    b = apply_step(p, Annotate("C", "i.0", "parallel"))
+    assert lower.lower(a).source == lower.lower(b).source
+    info = lower.lower(a).kernels[0].info
+    assert info["template"] == "tiled" and info["threads"] == 4 * 4 and info["blocks"] == 4 * 2 and info["vthreads"] == 2 * 2
+
+
+def test_reference_lowering_is_fp64():
+    lo = lower.reference_lowering(build("conv2d", h=6, w=6, ci=4, co=4))
+    assert "double" in lo.source and "float*" not in lo.source
+    assert [k.info["template"] for k in lo.kernels] == ["naive", "naive"]
+
+
+def test_library_loads_and_exports_header_symbols():
+    from paper_2006_06762_b200 import build as B
+    from paper_2006_06762_b200 import runtime as rt
+    B.build()
+    lib = ctypes.CDLL(B.LIB)
+    with open(os.path.join(ROOT, "include", "loomtune_b200.h")) as fh:
+        hdr = fh.read()
+    declared = set(re.findall(r"\b(lt_[a-z_0-9]+)\s*\(", hdr))
+    assert declared, "no declarations found"
+    for name in sorted(declared):
+        getattr(lib, name)  # raises AttributeError if not exported
+    assert set(rt.EXPORTS) <= declared
+    assert os.access(B.WORKER, os.X_OK)
+
+
+def test_nvrtc_pool_compiles_generated_kernel(tmp_path):
+    """The compile service works without a GPU (NVRTC cross-compiles sm_100a)."""
+    from paper_2006_06762_b200 import runtime as rt
+    from paper_2006_06762_b200.measure import NVRTC_OPTS
+    lib = rt.load(require_device=False)
+    rt.check(lib.lt_pool_start(2, str(tmp_path).encode(), 120.0), "pool")
+    try:
+        src = lower.lower(naive_program(build("matmul", n=16, m=16, k=16))).source.encode()
+        ids = [lib.lt_compile_submit(src, len(src), NVRTC_OPTS.encode()) for _ in range(2)]
+        for j in ids:
+            st, secs, hit, n = ctypes.c_int(), ctypes.c_double(), ctypes.c_int(), ctypes.c_int64()
+            rt.check(lib.lt_compile_wait(j, ctypes.byref(st), ctypes.byref(secs), ctypes.byref(hit),
+                                         ctypes.byref(n)), "wait")
+            buf = ctypes.create_string_buffer(n.value)
+            rt.check(lib.lt_compile_fetch(j, buf, n.value), "fetch")
+            assert st.value == 0 and buf.raw[:4] == b"\x7fELF"
+        # second submission of the same source is a cache hit
+        j = lib.lt_compile_submit(src, len(src), NVRTC_OPTS.encode())
+        st, secs, hit, n = ctypes.c_int(), ctypes.c_double(), ctypes.c_int(), ctypes.c_int64()
+        lib.lt_compile_wait(j, ctypes.byref(st), ctypes.byref(secs), ctypes.byref(hit), ctypes.byref(n))
+        lib.lt_compile_fetch(j, None, 0)
+        assert hit.value == 1
+    finally:
+        lib.lt_pool_stop()
+
+
+def test_pack_matches_reference_semantics():
+    from paper_2006_06762_b200.measure import pack
+    rng = np.random.default_rng(0)
+    B = rng.random((8, 12))
+    desc = ((1, 3), (0, 2), (1, 4), (0, 4))
+    P = pack(B, desc)
+    for a in range(3):
+        for b in range(2):
+            for c in range(4):
+                for d in range(4):
+                    assert P[a, b, c, d] == B[b * 4 + d, a * 4 + c]

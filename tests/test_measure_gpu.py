@@ -1,0 +1,126 @@
+"""GPU runner parity: every candidate the runner accepts computes the reference's outputs."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def runner():
+    from paper_2006_06762_b200 import measure
+    r = measure.configure(device=0, cache_dir="")
+    yield r
+
+
+def test_small_corpus_all_outputs_correct(corpus, runner):
+    from paper_2006_06762_b200.measure import VALID
+    small = [i for i, e in enumerate(corpus.entries) if ":" in e["dag"] and not e["dag"].startswith("tune")]
+    progs = [corpus.programs[i] for i in small]
+    recs = runner.measure_programs(progs)
+    n_valid = sum(r.status == VALID for r in recs)
+    wrong = [(small[k], r.detail) for k, r in enumerate(recs) if "differs from reference" in r.detail]
+    faults = [(small[k], r.detail) for k, r in enumerate(recs) if "compile failed" in r.detail]
+    assert not wrong, wrong[:5]
+    assert not faults, faults[:3]
+    assert n_valid >= 0.8 * len(progs), (n_valid, len(progs))
+    for r in recs:
+        if r.status == VALID:
+            assert r.max_rel_err <= 1e-4 and math.isfinite(r.cost_us) and r.cost_us > 0
+    print(f"small corpus: {n_valid}/{len(progs)} VALID")
+
+
+def test_evolved_states_correct(corpus, runner):
+    idx = [i for i, e in enumerate(corpus.entries) if e["dag"].startswith("tune")]
+    recs = runner.measure_programs([corpus.programs[i] for i in idx])
+    wrong = [(idx[k], r.detail) for k, r in enumerate(recs) if "differs" in r.detail or "compile failed" in r.detail]
+    assert not wrong, wrong[:5]
+
+
+def test_ground_truth_matches_reference_outputs(runner):
+    """The device fp64 ground truth equals the reference's `reference_outputs` (golden)."""
+    from paper_2006_06762_b200.state import build
+    outs = np.load(os.path.join(GOLDEN, "outputs.npz"))
+    shapes = {"matmul": dict(n=64, m=64, k=64), "conv2d": dict(h=6, w=6, ci=8, co=8, n=2),
+              "batch_matmul": dict(b=4, n=16, m=16, k=8), "conv_bn_relu": dict(n=2, h=6, w=6, ci=8, co=8),
+              "norm2": dict(n=8, m=32), "grouped_conv2d": dict(h=6, w=6, ci=8, co=8)}
+    for name, kw in shapes.items():
+        dag = build(name, **kw)
+        ctx = runner.context(dag, 0)
+        for o in dag.outputs:
+            want = outs[f"{name}/{o}"]
+            got = ctx.download(o, want.size, fp64=True).reshape(want.shape)
+            np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+
+
+def test_candidate_outputs_match_reference_outputs(corpus, runner):
+    """Download a candidate's fp32 output and compare with the golden reference outputs."""
+    from paper_2006_06762_b200.measure import VALID
+    outs = np.load(os.path.join(GOLDEN, "outputs.npz"))
+    checked = 0
+    for i, e in enumerate(corpus.entries):
+        name = e["dag"].split(":")[0]
+        if name not in ("matmul", "conv2d", "batch_matmul", "conv_bn_relu") or e["dag"].startswith("tune"):
+            continue
+        p = corpus.programs[i]
+        (rec,) = runner.measure_programs([p])
+        if rec.status != VALID:
+            continue
+        ctx = runner.context(p.dag, 0)
+        for o in p.dag.outputs:
+            want = outs[f"{name}/{o}"]
+            got = ctx.download(o, want.size).reshape(want.shape).astype(np.float64)
+            rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
+            assert float(rel.max()) <= 1e-4, (i, float(rel.max()))
+        checked += 1
+    assert checked >= 20
+
+
+def test_status_semantics_match_reference(runner):
+    """validate() failures carry the reference's detail; normalisation is the reference's."""
+    from paper_2006_06762_b200.measure import INVALID, VALID, measure_batch
+    from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
+    with open(os.path.join(GOLDEN, "corpus.json")) as fh:
+        dags = json.load(fh)["dags"]
+    with open(os.path.join(GOLDEN, "measure.json")) as fh:
+        cases = json.load(fh)
+    for case in cases:
+        dag = ComputeDAG.from_json(dags[case["dag"]])
+        progs = [replay(dag, history_from_json(h)) for h in case["histories"]]
+        res = measure_batch(progs)
+        for r, bad in zip(res, case["validate"]):
+            if bad:
+                assert r.status == INVALID and r.detail == bad[0] and r.cost == math.inf and r.throughput == 0.0
+        valid = [r for r in res if r.status == VALID]
+        best = min(r.cost for r in valid)
+        for r in valid:
+            assert r.throughput == best / r.cost
+        anchored = measure_batch(progs[:1], best_cost=best / 2)
+        if anchored[0].status == VALID:
+            assert anchored[0].throughput == (best / 2) / anchored[0].cost
+
+
+def test_timeout_ceiling(runner):
+    from paper_2006_06762_b200.measure import TIMEOUT, MeasureLimits, measure_batch
+    from paper_2006_06762_b200.state import build, naive_program
+    (r,) = measure_batch([naive_program(build("matmul", n=64, m=64, k=64))], limits=MeasureLimits(cost_ceiling=1e-3))
+    assert r.status == TIMEOUT and math.isfinite(r.cost) and r.throughput == 0.0
+
+
+def test_baseline_configs_measure(corpus, runner):
+    """BASELINE-shape States (G5, G10, RC, TBG, CL): every accepted candidate is correct."""
+    from paper_2006_06762_b200.measure import VALID
+    idx = [i for i, e in enumerate(corpus.entries) if e["dag"] in ("G5", "G10", "RC", "TBG", "CL")]
+    recs = runner.measure_programs([corpus.programs[i] for i in idx])
+    wrong = [(idx[k], r.detail) for k, r in enumerate(recs) if "differs" in r.detail or "compile failed" in r.detail]
+    assert not wrong, wrong[:5]
+    print("baseline configs:", sum(r.status == VALID for r in recs), "/", len(recs), "VALID")
+    for k, r in enumerate(recs):
+        if r.status == VALID:
+            print("  ", corpus.entries[idx[k]]["dag"], f"{r.cost_us:.1f} us", r.info["kernels"][0].get("template"))
