@@ -55,6 +55,7 @@ struct Worker {
 
 class Pool {
  public:
+  ~Pool() { stop(); }
   int start(int n, const std::string& cache_dir, double timeout_s);
   void stop();
   int64_t submit(const char* src, int64_t len, const char* opts);

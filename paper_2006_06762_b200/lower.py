@@ -185,6 +185,7 @@ class Emitter:
 
     def __init__(self, dtype: str, iv, read):
         self.dtype, self.iv, self.read = dtype, iv, read
+        self.guard = 0
 
     def __call__(self, e) -> str:
         k = kind(e)
@@ -194,7 +195,7 @@ class Emitter:
         if k == "IterVal":
             return f"(({d})({_lin(e.lin, self.iv)}))"
         if k == "Read":
-            return self.read(e.buffer, e.index)
+            return self.read(e.buffer, e.index, self.guard > 0)
         if k == "Bin":
             a, b = self(e.lhs), self(e.rhs)
             f = "f" if d == "float" else ""
@@ -208,8 +209,17 @@ class Emitter:
             f = "f" if d == "float" else ""
             return {"exp": f"exp{f}", "sqrt": f"sqrt{f}", "log": f"log{f}", "abs": f"fabs{f}"}[e.fn] + f"({self(e.arg)})"
         if k == "Select":
+            # Branch reads are only performed where the condition holds
+            # (src/expr.py:388-393); their indices may be negative elsewhere, which is
+            # why every global address is formed from sign-extended 64-bit terms.
             zero = "0.0f" if d == "float" else "0.0"
-            return f"(({self(e.cond)}) != {zero} ? ({self(e.then)}) : ({self(e.other)}))"
+            cond = self(e.cond)
+            self.guard += 1
+            try:
+                a, b = self(e.then), self(e.other)
+            finally:
+                self.guard -= 1
+            return f"(({cond}) != {zero} ? ({a}) : ({b}))"
         raise LoweringError(f"unsupported expression node {k}")
 
 
@@ -262,16 +272,18 @@ class _Ctx:
                 phys.append(f"({x} % {e})" if e < self.shape(name)[d] or st > 1 else x)
             flat, mul = [], 1
             for i in range(len(desc) - 1, -1, -1):
-                flat.append(phys[i] if mul == 1 else f"{phys[i]}*{mul}")
+                flat.append(f"(long long){phys[i]}" if mul == 1 else f"(long long){phys[i]}*{mul}")
                 mul *= desc[i][1]
             return f"__ldg(&{self.param(key)}[{' + '.join(reversed(flat))}])"
         if name not in self.live and name not in self.buffers:
             self.buffers[name] = Buffer(name, self.shape(name), "input")
         self._ref(name)
         shape = self.shape(name)
+        # 64-bit signed address arithmetic: unrolled loops share a base offset that
+        # can be negative even when every access is in bounds
         flat, mul = [], 1
         for d in range(len(shape) - 1, -1, -1):
-            flat.append(f"({idx_exprs[d]})" if mul == 1 else f"({idx_exprs[d]})*{mul}")
+            flat.append(f"(long long)({idx_exprs[d]})" if mul == 1 else f"(long long)({idx_exprs[d]})*{mul}")
             mul *= shape[d]
         addr = " + ".join(reversed(flat)) if flat else "0"
         return f"__ldg(&{self.param(name)}[{addr}])"
@@ -280,7 +292,7 @@ class _Ctx:
         shape = self.shape(name)
         flat, mul = [], 1
         for d in range(len(shape) - 1, -1, -1):
-            flat.append(f"({idx_exprs[d]})" if mul == 1 else f"({idx_exprs[d]})*{mul}")
+            flat.append(f"(long long)({idx_exprs[d]})" if mul == 1 else f"(long long)({idx_exprs[d]})*{mul}")
             mul *= shape[d]
         return f"{self.param(name)}[{' + '.join(reversed(flat)) if flat else '0'}] = {value};"
 
@@ -327,15 +339,17 @@ class _Ctx:
         attached_prod = {s.name for s in _attached(self.p, stage.name)
                          if _reads_buffer(stage.expr, s.name)}
 
-        def read(buf, index):
+        def read(buf, index, guarded=False):
             if override is not None:
                 r = override(buf, index)
                 if r is not None:
                     return r
-            idx = [_lin(l, lambda n: env[n]) for l in index]
             if buf in attached_prod:
-                return self.producer_call(buf, idx)
-            return self.global_load(buf, idx)
+                return self.producer_call(buf, [_lin(l, lambda n: env[n]) for l in index])
+            # global addresses: iterator leaves widened to 64 bits before any
+            # arithmetic, so a negative partial sum (padding reads under a Select)
+            # can never be zero-extended by the compiler
+            return self.global_load(buf, [_lin(l, lambda n: f"(long long){env[n]}") for l in index])
         return read
 
 
@@ -685,7 +699,7 @@ def _tiled_kernel(ctx: _Ctx, s, levels, entry: str) -> tuple:
     loc = {a: mixed(a, "S", 1) for a in space}
     loc.update({r: mixed(r, "R", 1) for r in red})
 
-    def smem_read(buf, index):
+    def smem_read(buf, index, guarded=False):
         key = (buf, tuple((l.terms, l.const) for l in index))
         o = next(o for o in operands if o["key"] == key)
         coords = []
@@ -740,10 +754,11 @@ def _tiled_kernel(ctx: _Ctx, s, levels, entry: str) -> tuple:
         for dd in range(len(hull) - 1, -1, -1):
             L.append(f"{ind}  const int c{dd}_ = c_ % {hull[dd]}; c_ /= {hull[dd]};")
         idx = [f"({o['base'][dd]}) + c{dd}_" for dd in range(len(hull))]
+        idx64 = [f"(long long)({o['base'][dd]}) + c{dd}_" for dd in range(len(hull))]
         if r.buffer in attached_prod:
             v = ctx.producer_call(r.buffer, idx)
         else:
-            v = ctx.global_load(r.buffer, idx)
+            v = ctx.global_load(r.buffer, idx64)
         L.append(f"{ind}  {o['name']}[e_] = {v};")
         L.append(f"{ind}}}")
     L.append(f"{ind}__syncthreads();")

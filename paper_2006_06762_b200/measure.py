@@ -19,6 +19,7 @@ ignored.  Inputs are `random_inputs(dag, default_rng(limits.check_seed))`
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import hashlib
 import json
@@ -166,7 +167,8 @@ class _DagContext:
                 L.arg_slot[a] = self.buffer_slot(lo.buffers[name], fp64)
         return arr
 
-    def measure(self, lo: Lowered, funcs: list, min_ms: float, max_repeat: int) -> rt.MeasureRecord:
+    def measure(self, lo: Lowered, funcs: list, min_ms: float, max_repeat: int,
+                min_repeat: int = 1) -> rt.MeasureRecord:
         launches = self._launches(lo, funcs)
         pairs, numel = [], []
         for name in lo.outputs:
@@ -178,7 +180,7 @@ class _DagContext:
         rec = rt.MeasureRecord()
         rt.check(self.r.lib.lt_measure(self.task, ctypes.addressof(launches), len(lo.kernels),
                                        rt.ptr(pairs_a, rt.c_i32p), rt.ptr(numel_a, rt.c_i64p), len(numel),
-                                       2, max_repeat, min_ms, ctypes.addressof(rec)), "lt_measure")
+                                       min_repeat, max_repeat, min_ms, ctypes.addressof(rec)), "lt_measure")
         return rec
 
     def download(self, name: str, numel: int, fp64: bool = False) -> np.ndarray:
@@ -192,7 +194,8 @@ class Runner:
     """Per-process GPU runner: one device, one compile pool, DAG contexts, module cache."""
 
     def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
-                 min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0):
+                 min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0,
+                 min_repeat: int = 1):
         self.lib = rt.load()
         self.device = device
         rt.check(self.lib.lt_set_device(device), "set device")
@@ -201,7 +204,7 @@ class Runner:
             "LT_CUBIN_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "loomtune_b200", "cubin"))
         rt.check(self.lib.lt_pool_start(self.workers, self.cache_dir.encode() if self.cache_dir else None,
                                         compile_timeout), "compile pool")
-        self.min_ms, self.max_repeat = min_ms, max_repeat
+        self.min_ms, self.max_repeat, self.min_repeat = min_ms, max_repeat, min_repeat
         self.ctx: dict = {}
         self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
         self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0}
@@ -300,7 +303,7 @@ class Runner:
                     continue
                 funcs = self.load(key, data, [k.entry for k in lo.kernels])
             ctx = self.context(p.dag, seed)
-            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat)
+            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
             self.stats["measured"] += 1
             rec.first_us, rec.repeats = m.first_us, m.repeats
             rec.max_rel_err = float(m.max_rel_err)
@@ -317,6 +320,16 @@ class Runner:
 
 
 _RUNNER: Runner | None = None
+
+
+def _shutdown() -> None:
+    global _RUNNER
+    if _RUNNER is not None:
+        _RUNNER.close()
+        _RUNNER = None
+
+
+atexit.register(_shutdown)
 
 
 def get_runner(**kw) -> Runner:
