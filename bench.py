@@ -1,0 +1,372 @@
+"""Headline benchmark: measured candidates/sec of the B200 measurement pipeline.
+
+A step = measuring one batch of fresh candidate States of the BASELINE config
+(default RC = ResNet-50 conv2d N16 56x56x64->64 3x3, BASELINE.json configs[1])
+through the drop-in `measure_batch`: validate -> lower -> NVRTC compile (empty
+cubin cache, exact constants) -> run on the B200 -> verify every output vs the
+fp64 ground truth on device -> time.  Candidates come from
+tests/golden/streams/<CFG>.json.gz (the reference's own sampler, filtered to
+legal launches); every step uses States never seen before in the run.
+
+Multi-GPU (torchrun): each rank measures its own disjoint slice of every step's
+batch (measurement units are independent); only the measured
+records are gathered (NCCL all_gather).  value = candidates of all ranks /
+max-over-ranks time.
+
+--impl reference times the reference's CPU runner (oracle/machine.py, a
+restatement of src/machine.py:249-285: validate + shrunken-twin interpretation
++ analytical cost) on the same candidates with all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import gzip
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FLOPS = {"RC": 2 * 16 * 56 * 56 * 64 * 64 * 9, "G10": 2 * 1024 ** 3, "G5": 2 * 512 ** 3,
+         "TBG": 2 * 192 * 128 * 128 * 64, "CL": 2 * 16 * 28 * 28 * 128 * 128 * 9}
+NAMES = {"RC": "ResNet-50 conv2d N16 56x56x64->64 3x3 s1", "G10": "GEMM 1024^3", "G5": "GEMM 512^3",
+         "TBG": "batched GEMM 192x128x128x64", "CL": "ConvLayer N16 28x28x128->128 3x3 + BN + ReLU"}
+
+
+def load_stream(cfg: str):
+    from paper_2006_06762_b200.state import ComputeDAG, history_from_json
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "streams", f"{cfg}.json.gz"), "rt") as fh:
+        data = json.load(fh)
+    return ComputeDAG.from_json(data["dag"]), [history_from_json(h) for h in data["histories"]]
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (the recipe's clocks line)."""
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, ValueError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        busy = [r for r in rows if r[7].isdigit() and int(r[7]) > 0] or rows
+        mhz = [float(r[0]) for r in busy if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in busy for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(mhz) if mhz else None,
+                "sm_max_mhz": float(rows[0][1]) if rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(busy)}
+
+
+def cpu_reference(histories, dag, seconds: float, cores: int) -> dict:
+    """The reference's CPU runner restated (oracle/machine.py) over a bounded
+    sample, parallel over host cores; returns candidates/sec."""
+    from concurrent.futures import ProcessPoolExecutor
+    from paper_2006_06762_b200.state import history_to_json
+    items = [(json.dumps(dag.to_json()), history_to_json(h)) for h in histories]
+    t0 = time.perf_counter()
+    done = 0
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        futs = [ex.submit(_cpu_one, it) for it in items[: max(cores * 2, 4)]]
+        for f in futs:
+            f.result()
+            done += 1
+        # keep feeding until the time budget is used
+        k = len(futs)
+        while time.perf_counter() - t0 < seconds and k < len(items):
+            batch = [ex.submit(_cpu_one, it) for it in items[k: k + cores]]
+            k += len(batch)
+            for f in batch:
+                f.result()
+                done += 1
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "candidates": done, "seconds": dt}
+
+
+def _cpu_one(item):
+    sys.path.insert(0, ROOT)
+    from oracle import machine as OM
+    from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
+    dag_json, hist = item
+    p = replay(ComputeDAG.from_json(json.loads(dag_json)), history_from_json(hist))
+    return OM.measure_batch([p])[0].status
+
+
+def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
+    """Population scoring (features + trees) over a synthetic population of 2^16
+    programs (replicated stream States): device-resident kernel times and the
+    host e2e rate."""
+    import numpy as np
+    import torch
+    from paper_2006_06762_b200 import runtime as rt
+    from paper_2006_06762_b200.encode import encode_batch
+    from paper_2006_06762_b200.model import GpuCostModel
+    lib = rt.load()
+    model = GpuCostModel.from_json(json.load(open(os.path.join(ROOT, "tests", "golden", "model.json"))))
+    base_words, base_off, base_prog = encode_batch(programs)
+    n_rep = max(1, (1 << 16) // len(programs))
+    words = np.tile(base_words, n_rep)
+    stmt_off = np.concatenate([base_off[:-1] + i * len(base_words) for i in range(n_rep)] + [[len(words)]])
+    prog_off = np.concatenate([base_prog[:-1] + i * base_prog[-1] for i in range(n_rep)]
+                              + [[base_prog[-1] * n_rep]]).astype(np.int64)
+    n_stmt, n_prog = len(stmt_off) - 1, len(prog_off) - 1
+    dev = torch.device("cuda", runner_dev)
+    d_words = torch.from_numpy(words).to(dev)
+    d_soff = torch.from_numpy(stmt_off).to(dev)
+    d_poff = torch.from_numpy(prog_off).to(dev)
+    d_rows = torch.empty((n_stmt, 164), dtype=torch.float64, device=dev)
+    d_rs = torch.empty(n_stmt, dtype=torch.float64, device=dev)
+    d_sc = torch.empty(n_prog, dtype=torch.float64, device=dev)
+    d_err = torch.zeros(1, dtype=torch.int32, device=dev)
+    h = model.handle()
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def feats():
+        rt.check(lib.lt_features_device(d_words.data_ptr(), d_soff.data_ptr(), n_stmt, d_rows.data_ptr(),
+                                        d_err.data_ptr(), sp), "features")
+
+    def trees():
+        rt.check(lib.lt_predict_rows_device(h, d_rows.data_ptr(), n_stmt, d_rs.data_ptr(), sp), "trees")
+        rt.check(lib.lt_segment_sum_device(d_rs.data_ptr(), d_poff.data_ptr(), n_prog, d_sc.data_ptr(), sp), "sum")
+
+    out = {}
+    for name, fn in (("features", feats), ("trees", trees)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        out[name + "_ms"] = e0.elapsed_time(e1) / reps
+    # host e2e: encode + H2D + fused scoring + D2H through the public API
+    t0 = time.perf_counter()
+    sc = model.predict_batch(programs * n_rep)
+    out["e2e_s"] = time.perf_counter() - t0
+    out.update(n_prog=n_prog, n_stmt=n_stmt, words_bytes=int(words.nbytes), scores_finite=bool(np.isfinite(sc).all()))
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="RC", choices=sorted(FLOPS))
+    ap.add_argument("--batch", type=int, default=24, help="candidates per rank per step")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-scoring", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dag, stream = load_stream(args.config)
+    cores = os.cpu_count() or 1
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        per_step = []
+        for s in range(args.warmup + args.steps):
+            sample = stream[s * cores:(s + 1) * cores * 4]
+            r = cpu_reference(sample, dag, args.cpu_seconds / 2, cores)
+            if s >= args.warmup:
+                per_step.append(r)
+        tot_c = sum(r["candidates"] for r in per_step)
+        tot_s = sum(r["seconds"] for r in per_step)
+        v = tot_c / tot_s
+        print(json.dumps({
+            "impl": "reference", "metric": f"measured candidates/sec ({args.config}, SSSRRSRS)", "value": v,
+            "unit": "cand/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tot_s / len(per_step), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": NAMES[args.config], "stream": f"tests/golden/streams/{args.config}.json.gz"},
+            "cpu_baseline": {"value": v, "unit": "cand/s", "cores": cores, "kind": "port",
+                             "sample": f"{tot_c} stream States; oracle/machine.py measure_batch "
+                                       "(validate + twin interpret + machine_cost) in a process pool"},
+            "e2e": {"value": v, "unit": "cand/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    from paper_2006_06762_b200 import measure
+    from paper_2006_06762_b200 import runtime as rt
+    from paper_2006_06762_b200.state import replay
+
+    workers = max(1, cores // world - (1 if world == 1 else 0))
+    cache = tempfile.mkdtemp(prefix="lt_cubin_")     # empty: every candidate really compiles
+    runner = measure.configure(device=local, workers=workers, cache_dir=cache)
+    runner.context(dag, 0)                             # inputs + fp64 ground truth resident
+
+    B = args.batch
+    need = (args.warmup + 2 * args.steps) * B * world
+    if need > len(stream):
+        raise SystemExit(f"stream has {len(stream)} States, run needs {need}")
+
+    def batch(step: int):
+        lo = (step * world + rank) * B
+        return [replay(dag, h) for h in stream[lo:lo + B]]
+
+    def sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    all_recs = []
+    launch_log = []
+
+    def run_steps(first: int, n: int, fresh_ctx: bool) -> float:
+        """Time n steps with CUDA events on the current stream; max over ranks."""
+        progs = [batch(first + s) for s in range(n)]
+        sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for ps in progs:
+            if fresh_ctx:   # e2e: inputs re-uploaded and ground truth recomputed inside the region
+                for c in runner.ctx.values():
+                    runner.lib.lt_task_destroy(c.task)
+                runner.ctx.clear()
+            res = measure.measure_batch(ps)
+            all_recs.append(res)
+            launch_log.append(list(runner.last_records))
+        e1.record()
+        sync()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    run_steps(0, args.warmup, False)                               # warm-up (NVRTC workers, clocks)
+    runner.stats.update({"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0})
+    with Clocks(local) as clk:
+        ms = run_steps(args.warmup, args.steps, False)
+    stats = dict(runner.stats)
+    timed = all_recs[-args.steps:]
+    timed_records = [r for step in launch_log[-args.steps:] for r in step]
+    # our kernels launched in the timed region: per measured candidate, its kernels x
+    # (warm-up + repeats), plus one NaN-poison and one verification launch per output
+    n_launch = sum(len(r.info.get("kernels", [])) * (1 + r.repeats) + 2 * r.n_outputs
+                   for r in timed_records if r.repeats)
+    e2e_ms = run_steps(args.warmup + args.steps, args.steps, True)
+
+    # gather measured records (status, cost) over NCCL: the only cross-rank exchange
+    flat = [(1.0 if r.status == "valid" else 0.0, r.cost if math.isfinite(r.cost) else -1.0)
+            for rs in timed for r in rs]
+    mine = torch.tensor(flat, dtype=torch.float64, device="cuda")
+    if world > 1:
+        bufs = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(bufs, mine)
+        gathered = torch.cat(bufs).cpu().numpy()
+    else:
+        gathered = mine.cpu().numpy()
+    n_total = len(gathered)
+    n_valid = int(gathered[:, 0].sum())
+    costs = gathered[gathered[:, 0] > 0, 1]
+    best_us = float(costs.min()) if len(costs) else float("nan")
+    value = n_total / (ms / 1000.0)
+    e2e = (args.steps * B * world) / (e2e_ms / 1000.0)
+
+    if rank == 0:
+        lib = rt.load()
+        import ctypes
+        tf, pms = ctypes.c_double(), ctypes.c_double()
+        rt.check(lib.lt_ffma_peak(local, ctypes.byref(tf), ctypes.byref(pms)), "ffma peak")
+        peak = tf.value
+        achieved = FLOPS[args.config] / (best_us * 1e-6) / 1e12 if math.isfinite(best_us) else None
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        except (OSError, ValueError):
+            pass
+        line = {
+            "metric": f"measured candidates/sec ({args.config}, SSSRRSRS, compile+run+verify)",
+            "value": value, "unit": "cand/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": NAMES[args.config], "candidates_per_rank_per_step": B,
+                       "stream": f"tests/golden/streams/{args.config}.json.gz (reference sampler, legal launches)",
+                       "compile_workers_per_rank": workers, "cubin_cache": "empty at start",
+                       "l2": "inputs resident; no flush between repeats (Ansor measurement semantics)"},
+            "valid": n_valid, "measured": n_total,
+            "best_program": {"us": best_us, "tflops": achieved, "flop": FLOPS[args.config]},
+            "compile": {"compiled": stats["compiled"], "cache_hits": stats["cache_hits"],
+                        "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
+            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "kernel": "best candidate of the timed steps (cost = mean of CUDA-event repeats)",
+                         "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU"},
+            "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                    "note": "fresh DAG context per step: inputs H2D + fp64 ground truth inside the region"},
+            "gpu_launches": n_launch,
+        }
+        line["clocks"] = clk.summary()
+        if not args.no_scoring:
+            progs = [replay(dag, h) for h in stream[:256]]
+            sb = scoring_bench(local, progs)
+            rows_bytes = sb["n_stmt"] * 164 * 8
+            fbytes = sb["words_bytes"] + rows_bytes
+            hbm = peaks.get("hbm_gbs")
+            line["scoring"] = {
+                "programs": sb["n_prog"], "statements": sb["n_stmt"],
+                "device_programs_per_s": sb["n_prog"] / ((sb["features_ms"] + sb["trees_ms"]) / 1000),
+                "e2e_programs_per_s": sb["n_prog"] / sb["e2e_s"],
+                "features_ms": sb["features_ms"], "trees_ms": sb["trees_ms"],
+                "roofline_features": {"bound": "hbm", "achieved": fbytes / (sb["features_ms"] / 1000) / 1e9,
+                                      "peak": hbm, "unit": "GB/s",
+                                      "frac": (fbytes / (sb["features_ms"] / 1000) / 1e9) / hbm if hbm else None,
+                                      "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
+        # CPU baseline: the reference's runner restated, bounded sample, all host cores
+        cb = cpu_reference(stream[-cores * 8:], dag, args.cpu_seconds, cores)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": "cand/s", "cores": cores, "kind": "port",
+                                "sample": f"{cb['candidates']} stream States through oracle/machine.py "
+                                          "measure_batch (validate + twin interpret + machine_cost)"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -193,7 +193,7 @@ def _buffer_shape(p, name):
     return p.dag.node(name).shape
 
 
-def analyze(p) -> list:
+def analyze(p, with_present: bool = True) -> list:
     """One dict per live statement, fields as `StatementAnalysis`."""
     layouts = dict(p.layouts)
     live = [s for s in p.stages if not s.inlined]
@@ -254,7 +254,7 @@ def analyze(p) -> list:
                 a0 = sum(clip(evaluate(d, e0), n) * f for (d, n), f in zip(dims, fs))
                 a1 = sum(clip(evaluate(d, e1), n) * f for (d, n), f in zip(dims, fs))
                 stride = abs(a1 - a0) * ELEM_BYTES
-            acc_list.append(dict(buffer=buf, acc=acc, total_bytes=tb, unique_bytes=ub,
+            acc_list.append(dict(buffer=buf, acc=acc, present=present, total_bytes=tb, unique_bytes=ub,
                                  lines=tb / LINE_BYTES, unique_lines=ul, reuse=rt, counter=cnt,
                                  dist_iters=di, dist_bytes=db, stride=stride))
         ws = []

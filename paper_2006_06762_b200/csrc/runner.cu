@@ -364,3 +364,53 @@ int lt_measure(int64_t handle, const lt_launch* launches, int n_launch, const in
 }
 
 }  // extern "C"
+
+// ---- FP32 FFMA peak (the roofline denominator for candidate kernels) --------
+// 8 independent FFMA chains per thread, 8 resident warps per SMSP: issue-bound.
+namespace lt {
+__global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, float m, float c) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = (float)(threadIdx.x + k) * 1e-3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], m, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 123.456f) out[threadIdx.x] = s;   // keep the chains live
+}
+}  // namespace lt
+
+extern "C" int lt_ffma_peak(int device, double* tflops, double* ms_out) {
+  if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return -1;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* out = nullptr;
+  if (lt::check_cuda(cudaMalloc(&out, 1024 * sizeof(float)), "cudaMalloc")) return -1;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  lt::ffma_peak_kernel<<<blocks, threads>>>(out, 64, 0.9999f, 1e-4f);   // warm-up / clocks up
+  double best = 1e30;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    lt::ffma_peak_kernel<<<blocks, threads>>>(out, iters, 0.9999f, 1e-4f);
+    cudaEventRecord(e1);
+    if (lt::check_cuda(cudaEventSynchronize(e1), "ffma peak")) return -1;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  double flops = 2.0 * (double)blocks * threads * iters * 16 * 8;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  *ms_out = best;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  return 0;
+}

@@ -70,6 +70,7 @@ class Record:
     compile_s: float = 0.0
     cache_hit: bool = False
     lower_s: float = 0.0
+    n_outputs: int = 0
     info: dict = field(default_factory=dict)
 
 
@@ -208,6 +209,7 @@ class Runner:
         self.ctx: dict = {}
         self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
         self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0}
+        self.last_records: list = []
 
     def close(self):
         for m, _ in self.modules.values():
@@ -306,6 +308,7 @@ class Runner:
             m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
             self.stats["measured"] += 1
             rec.first_us, rec.repeats = m.first_us, m.repeats
+            rec.n_outputs = len(lo.outputs)
             rec.max_rel_err = float(m.max_rel_err)
             if m.status != 0:
                 rec.detail = "gpu: " + m.detail.decode(errors="replace")
@@ -316,6 +319,7 @@ class Runner:
                 continue
             rec.status = VALID
             rec.cost_us = m.cost_us
+        self.last_records = recs
         return recs
 
 

@@ -35,3 +35,49 @@ def test_onehot_mask_matches_layout():
     assert len(names) == 164
     want = np.array([("_pos_" in n or "_acc_" in n or "_reuse_" in n) for n in names])
     assert (OF.ONEHOT == want).all()
+
+
+def test_oracle_reference_outputs_match_golden():
+    import os
+    from oracle import interp as OI
+    from paper_2006_06762_b200.state import build
+    from tests.tools_shapes import SMALL
+    outs = np.load(os.path.join(os.path.dirname(__file__), "golden", "outputs.npz"))
+    for name, kw in SMALL.items():
+        dag = build(name, **kw)
+        got = OI.reference_outputs(dag, OI.random_inputs(dag, np.random.default_rng(0)), chunk=1 << 12)
+        for o, arr in got.items():
+            np.testing.assert_allclose(arr, outs[f"{name}/{o}"], rtol=1e-13, atol=0)
+
+
+def test_oracle_interpret_matches_ground_truth(corpus):
+    """Every corpus State at small shape interprets to the reference ground truth."""
+    from oracle import interp as OI
+    for i, (p, e) in enumerate(zip(corpus.programs, corpus.entries)):
+        if ":" not in e["dag"] or i % 3:
+            continue
+        ins = OI.random_inputs(p.dag, np.random.default_rng(0))
+        got = OI.interpret(p, ins)
+        want = OI.reference_outputs(p.dag, ins)
+        for o in want:
+            err = np.max(np.abs(got[o] - want[o]) / np.maximum(np.abs(want[o]), 1e-30))
+            assert err <= 1e-9, (i, e["dag"], err)
+
+
+def test_oracle_measure_batch_matches_reference(corpus):
+    """Statuses, details, exact analytical costs and throughputs of the reference."""
+    import json
+    import math
+    import os
+    from oracle import machine as OM
+    from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
+    with open(os.path.join(os.path.dirname(__file__), "golden", "measure.json")) as fh:
+        cases = json.load(fh)
+    for case in cases:
+        dag = corpus.dags[case["dag"]]
+        progs = [replay(dag, history_from_json(h)) for h in case["histories"]]
+        res = OM.measure_batch(progs)
+        for r, (cost, thr, status, detail) in zip(res, case["results"]):
+            assert r.status == status and r.detail == detail
+            assert (r.cost == math.inf) if cost == "inf" else (r.cost == cost)
+            assert r.throughput == thr
