@@ -189,7 +189,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="RC", choices=sorted(FLOPS))
-    ap.add_argument("--batch", type=int, default=24, help="candidates per rank per step")
+    ap.add_argument("--batch", type=int, default=32, help="candidates per rank per step")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-scoring", action="store_true")
     args = ap.parse_args()

@@ -61,6 +61,11 @@ class Pool {
   int64_t submit(const char* src, int64_t len, const char* opts);
   int wait(int64_t id, int* status, double* secs, int* hit, int64_t* len);
   int fetch(int64_t id, char* buf, int64_t cap);
+  int ready(int64_t id) {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = jobs_.find(id);
+    return it == jobs_.end() ? -1 : (it->second.state == 2 ? 1 : 0);
+  }
   int size() const { return (int)workers_.size(); }
 
  private:
@@ -400,6 +405,9 @@ int64_t lt_compile_submit(const char* src, int64_t len, const char* opts) { retu
 int lt_compile_wait(int64_t job, int* status, double* secs, int* cache_hit, int64_t* out_len) {
   return lt::g_pool.wait(job, status, secs, cache_hit, out_len);
 }
+
+// 1 when the job has finished (wait/fetch will not block), 0 if not, -1 if unknown.
+int lt_compile_ready(int64_t job) { return lt::g_pool.ready(job); }
 
 // Copy the finished job's output (cubin, or the compile log on failure) and release the job.
 int lt_compile_fetch(int64_t job, char* buf, int64_t cap) { return lt::g_pool.fetch(job, buf, cap); }

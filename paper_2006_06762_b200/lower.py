@@ -27,9 +27,11 @@ CPU-only decisions (which loops are fused into the `parallel` band,
 two States that differ only there lower to the same source and share a cubin.
 
 GPU legality (reported as INVALID with a detail string, the reference's
-status for a program that cannot run): threads/block <= 1024, shared memory
-<= 227 KB, accumulators/thread <= MAX_ACC, vthreads <= MAX_VTHREAD, unrolled
-statements <= MAX_UNROLLED.  Values are computed in fp32 (FFMA), the paper's
+status for a program that cannot run): threads/block <= 1024 and shared memory
+<= 227 KB (hardware); virtual threads <= 8 (TVM's CUDA `max_vthread_extent`,
+the bound Ansor's GPU search and `verify_gpu_code` apply); accumulators/thread
+<= 256 (the 255-register file: a larger tile cannot be register-resident);
+unrolled statements <= 4096 (compile-time guard).  Values are computed in fp32 (FFMA), the paper's
 search space having no tensor cores.
 """
 
@@ -43,9 +45,9 @@ from .state.expr import kind, reads
 
 MAX_THREADS = 1024
 MAX_SMEM = 227 * 1024
-MAX_ACC = 1024
-MAX_VTHREAD = 64
-MAX_UNROLLED = 8192
+MAX_ACC = 256
+MAX_VTHREAD = 8
+MAX_UNROLLED = 4096
 NAIVE_THREADS = 256
 
 

@@ -269,6 +269,23 @@ class Runner:
                 out.append(self.load(hashlib.sha1(s.encode()).hexdigest(), data, e))
         return out
 
+    def _completion_order(self, pending: list):
+        """Yield pending candidates as their compiles finish (cached ones first)."""
+        ready = [x for x in pending if x[4] is None]
+        waiting = [x for x in pending if x[4] is not None]
+        for x in ready:
+            yield x
+        while waiting:
+            done = None
+            for k, x in enumerate(waiting):
+                if self.lib.lt_compile_ready(x[4]):
+                    done = k
+                    break
+            if done is None:
+                time.sleep(0.002)
+                continue
+            yield waiting.pop(done)
+
     # -- measurement ---------------------------------------------------------
     def measure_programs(self, programs: list, seed: int = 0) -> list:
         recs = [Record() for _ in programs]
@@ -290,7 +307,9 @@ class Runner:
             key = hashlib.sha1(lo.source.encode()).hexdigest()
             job = None if key in self.modules else self.submit(lo.source)
             pending.append((i, p, lo, key, job))
-        for i, p, lo, key, job in pending:
+        # measure in compile-completion order so the GPU overlaps the slowest compiles
+        order = self._completion_order(pending)
+        for i, p, lo, key, job in order:
             rec = recs[i]
             if job is None:
                 funcs = self.load(key, b"", [k.entry for k in lo.kernels])

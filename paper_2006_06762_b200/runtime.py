@@ -53,6 +53,7 @@ _SIGS = [
     ("lt_compile_submit", ctypes.c_int64, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_char_p]),
     ("lt_compile_wait", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]),
+    ("lt_compile_ready", ctypes.c_int, [ctypes.c_int64]),
     ("lt_compile_fetch", ctypes.c_int, [ctypes.c_int64, ctypes.c_char_p, ctypes.c_int64]),
     # runner (csrc/runner.cu)
     ("lt_module_load", ctypes.c_int64, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int64]),
