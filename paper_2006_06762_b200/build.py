@@ -68,7 +68,8 @@ def build(verbose: bool = False) -> str:
     wsrc = os.path.join(CSRC, "nvrtc_worker.cpp")
     if os.path.exists(wsrc) and _stale(WORKER, [wsrc] + headers):
         _run(["g++", "-O2", "-std=c++17", "-I", os.path.join(CUDA, "include"), wsrc, "-o", WORKER,
-              "-L", os.path.join(CUDA, "lib64"), "-lnvrtc", "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
+              "-L", os.path.join(CUDA, "lib64"), "-lnvrtc", "-lnvptxcompiler_static", "-lpthread", "-lm",
+              "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
     return LIB
 
 

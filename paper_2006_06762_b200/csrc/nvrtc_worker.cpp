@@ -6,9 +6,12 @@
 //   request : u32 n_opts, n_opts x (u32 len, bytes), u32 src_len, src bytes
 //   response: i32 status (0 ok, else nvrtcResult or -1), f64 seconds,
 //             u32 len, bytes (cubin when ok, compile log otherwise)
-// The worker exits when stdin closes.
+// The worker exits when stdin closes.  When the first option is "--ptx" the
+// source is PTX and is assembled in-process with nvPTXCompiler (ptxas as a
+// library) using the remaining options.
 
 #include <nvrtc.h>
+#include <nvPTXCompiler.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -59,6 +62,34 @@ int main() {
     auto t0 = std::chrono::steady_clock::now();
     int32_t status = 0;
     std::string out;
+    if (!opts.empty() && opts[0] == "--ptx") {
+      nvPTXCompilerHandle h = nullptr;
+      nvPTXCompileResult r = nvPTXCompilerCreate(&h, src.size(), src.data());
+      if (r == NVPTXCOMPILE_SUCCESS) {
+        std::vector<const char*> argv;
+        for (size_t i = 1; i < opts.size(); ++i) argv.push_back(opts[i].c_str());
+        r = nvPTXCompilerCompile(h, (int)argv.size(), argv.data());
+        if (r == NVPTXCOMPILE_SUCCESS) {
+          size_t n = 0;
+          nvPTXCompilerGetCompiledProgramSize(h, &n);
+          out.resize(n);
+          if (n) nvPTXCompilerGetCompiledProgram(h, &out[0]);
+        } else {
+          size_t n = 0;
+          nvPTXCompilerGetErrorLogSize(h, &n);
+          out.resize(n);
+          if (n) nvPTXCompilerGetErrorLog(h, &out[0]);
+        }
+      }
+      status = (int32_t)r;
+      if (h) nvPTXCompilerDestroy(&h);
+      double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      uint32_t len = (uint32_t)out.size();
+      if (!write_all(&status, 4) || !write_all(&secs, 8) || !write_all(&len, 4) ||
+          (len && !write_all(out.data(), len)))
+        return 0;
+      continue;
+    }
     nvrtcProgram prog;
     nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "candidate.cu", 0, nullptr, nullptr);
     if (r != NVRTC_SUCCESS) {

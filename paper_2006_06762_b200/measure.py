@@ -33,11 +33,13 @@ import numpy as np
 
 from . import runtime as rt
 from .lower import Lowered, LoweringError, lower, reference_lowering
+from .ptxgen import Unsupported, lower_ptx
 from .state.ir import validate
 
 VALID, INVALID, TIMEOUT = "valid", "invalid", "timeout"
 GPU_TOL = 1e-4
 NVRTC_OPTS = "--gpu-architecture=sm_100a\n-default-device\n-lineinfo"
+PTX_OPTS = "--ptx\n--gpu-name=sm_100a\n-O3"
 
 
 @dataclass(frozen=True)
@@ -196,7 +198,7 @@ class Runner:
 
     def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
                  min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0,
-                 min_repeat: int = 1):
+                 min_repeat: int = 1, backend: str = "ptx"):
         self.lib = rt.load()
         self.device = device
         rt.check(self.lib.lt_set_device(device), "set device")
@@ -206,6 +208,7 @@ class Runner:
         rt.check(self.lib.lt_pool_start(self.workers, self.cache_dir.encode() if self.cache_dir else None,
                                         compile_timeout), "compile pool")
         self.min_ms, self.max_repeat, self.min_repeat = min_ms, max_repeat, min_repeat
+        self.backend = backend
         self.ctx: dict = {}
         self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
         self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0}
@@ -229,7 +232,17 @@ class Runner:
     # -- compile + load ------------------------------------------------------
     def submit(self, source: str) -> int:
         b = source.encode()
-        return self.lib.lt_compile_submit(b, len(b), NVRTC_OPTS.encode())
+        opts = PTX_OPTS if source.startswith(".version") else NVRTC_OPTS
+        return self.lib.lt_compile_submit(b, len(b), opts.encode())
+
+    def lower(self, p) -> Lowered:
+        """PTX backend by default; NVRTC (CUDA C) for what PTX does not express."""
+        if self.backend == "ptx":
+            try:
+                return lower_ptx(p)
+            except Unsupported:
+                pass
+        return lower(p)
 
     def collect(self, job: int):
         st, secs, hit, n = ctypes.c_int(), ctypes.c_double(), ctypes.c_int(), ctypes.c_int64()
@@ -297,7 +310,7 @@ class Runner:
                 continue
             t0 = time.perf_counter()
             try:
-                lo = lower(p)
+                lo = self.lower(p)
             except LoweringError as e:
                 recs[i].detail = f"gpu: {e}"
                 recs[i].lower_s = time.perf_counter() - t0

@@ -1,0 +1,1029 @@
+"""Direct PTX backend for the candidate templates (no NVVM).
+
+NVRTC spends 80-90% of a candidate's compile in NVVM (C++ -> PTX); ptxas alone
+is 5-10x faster.  This module emits PTX for exactly the templates `lower.py`
+defines in CUDA C (same binding, staging, loop order, unroll coverage,
+epilogues, legality), so a candidate only pays for ptxas.  It performs the
+optimisations NVVM would otherwise do for these kernels: affine address
+arithmetic folded into `[reg + imm]` forms, value numbering of address and
+shared-memory loads inside straight-line regions, magic-number division by
+constants (ptxas emits a generic reciprocal sequence for `div.u32` by an
+immediate), fused multiply-add for sum-of-products reductions, predicated loads
+for `Select` branches.
+
+Unsupported constructs (math calls whose PTX approximations would not meet the
+1e-4 contract: exp/log) raise `Unsupported`; the runner then uses the NVRTC
+path for that candidate.  `tests/test_ptx_gpu.py` checks both backends produce
+identical verdicts and outputs.
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+
+from .lower import (
+    MAX_ACC, MAX_SMEM, MAX_THREADS, MAX_UNROLLED, MAX_VTHREAD, NAIVE_THREADS, Buffer, Kernel,
+    Lowered, LoweringError, _attached, _binding, _must_materialize, _reads_buffer, _unroll_flags,
+    _written, ident, tile_levels,
+)
+from .state.expr import kind, reads
+
+
+class Unsupported(Exception):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# affine integer forms over registers
+# ---------------------------------------------------------------------------
+
+
+class Aff:
+    __slots__ = ("terms", "const")
+
+    def __init__(self, terms=None, const=0):
+        self.terms = {r: c for r, c in (terms or {}).items() if c}
+        self.const = int(const)
+
+    @staticmethod
+    def reg(r, c=1):
+        return Aff({r: c})
+
+    @staticmethod
+    def k(c):
+        return Aff({}, c)
+
+    def __add__(self, o):
+        if isinstance(o, int):
+            return Aff(self.terms, self.const + o)
+        t = dict(self.terms)
+        for r, c in o.terms.items():
+            t[r] = t.get(r, 0) + c
+        return Aff(t, self.const + o.const)
+
+    def scale(self, s):
+        return Aff({r: c * s for r, c in self.terms.items()}, self.const * s)
+
+    def runtime(self):
+        return Aff(self.terms, 0)
+
+    def key(self):
+        return tuple(sorted(self.terms.items()))
+
+
+def _magic(d):
+    L = (d - 1).bit_length()
+    return -(-(1 << (31 + L)) // d), L - 1
+
+
+def _f32(x) -> str:
+    return "0f%08X" % struct.unpack("<I", struct.pack("<f", float(x)))[0]
+
+
+def _f64(x) -> str:
+    return "0d%016X" % struct.unpack("<Q", struct.pack("<d", float(x)))[0]
+
+
+class Ptx:
+    """One kernel's instruction stream with scoped value numbering."""
+
+    def __init__(self, dtype: str):
+        self.ft = "f32" if dtype == "float" else "f64"
+        self.fr = "%f" if self.ft == "f32" else "%fd"
+        self.esz = 4 if self.ft == "f32" else 8
+        self.n = {"%r": 0, "%rd": 0, "%p": 0, self.fr: 0}
+        self.lines: list = []
+        self.scopes: list = [{}]
+        self.labels = 0
+
+    def new(self, cls: str) -> str:
+        self.n[cls] += 1
+        return f"{cls}{self.n[cls]}"
+
+    def __call__(self, s: str) -> None:
+        self.lines.append("  " + s)
+
+    def label(self, name: str) -> None:
+        self.lines.append(f"{name}:")
+
+    def new_label(self) -> str:
+        self.labels += 1
+        return f"L{self.labels}"
+
+    def fconst(self, x) -> str:
+        return _f32(x) if self.ft == "f32" else _f64(x)
+
+    # value numbering
+    def cached(self, key):
+        for sc in reversed(self.scopes):
+            if key in sc:
+                return sc[key]
+        return None
+
+    def remember(self, key, val):
+        self.scopes[-1][key] = val
+        return val
+
+    def push(self):
+        self.scopes.append({})
+
+    def pop(self):
+        self.scopes.pop()
+
+    # integer arithmetic
+    def aff(self, a: Aff) -> str:
+        key = ("aff", a.key(), a.const)
+        hit = self.cached(key)
+        if hit:
+            return hit
+        r = None
+        for reg, c in sorted(a.terms.items()):
+            if r is None:
+                if c == 1:
+                    r = reg
+                else:
+                    r = self.new("%r")
+                    self(f"mul.lo.s32 {r}, {reg}, {c};")
+            else:
+                nr = self.new("%r")
+                self(f"mad.lo.s32 {nr}, {reg}, {c}, {r};")
+                r = nr
+        if r is None:
+            r = self.new("%r")
+            self(f"mov.s32 {r}, {a.const};")
+        elif a.const:
+            nr = self.new("%r")
+            self(f"add.s32 {nr}, {r}, {a.const};")
+            r = nr
+        return self.remember(key, r)
+
+    def udiv(self, x: str, d: int) -> str:
+        if d == 1:
+            return x
+        key = ("div", x, d)
+        hit = self.cached(key)
+        if hit:
+            return hit
+        r = self.new("%r")
+        if d & (d - 1) == 0:
+            self(f"shr.u32 {r}, {x}, {d.bit_length() - 1};")
+        else:
+            m, s = _magic(d)
+            self(f"mul.hi.u32 {r}, {x}, {m};")
+            if s:
+                self(f"shr.u32 {r}, {r}, {s};")
+        return self.remember(key, r)
+
+    def urem(self, x: str, d: int) -> str:
+        if d == 1:
+            return self.aff(Aff.k(0))
+        key = ("rem", x, d)
+        hit = self.cached(key)
+        if hit:
+            return hit
+        r = self.new("%r")
+        if d & (d - 1) == 0:
+            self(f"and.b32 {r}, {x}, {d - 1};")
+        else:
+            q = self.udiv(x, d)
+            self(f"mad.lo.s32 {r}, {q}, {-d}, {x};")
+        return self.remember(key, r)
+
+    def decompose(self, x: str, radices: list) -> list:
+        """Mixed-radix digits of x (last radix fastest)."""
+        out = [None] * len(radices)
+        cur = x
+        for i in range(len(radices) - 1, -1, -1):
+            d = radices[i]
+            if i == 0:
+                out[i] = cur
+            else:
+                out[i] = self.urem(cur, d)
+                cur = self.udiv(cur, d)
+        return out
+
+    def gaddr(self, base: str, flat: Aff) -> tuple:
+        """(64-bit base register, byte immediate) for element `flat` of a global buffer."""
+        rt = flat.runtime()
+        key = ("gaddr", base, rt.key())
+        hit = self.cached(key)
+        if hit is None:
+            if rt.terms:
+                off = self.aff(rt)
+                w = self.new("%rd")
+                self(f"mul.wide.s32 {w}, {off}, {self.esz};")
+                hit = self.new("%rd")
+                self(f"add.s64 {hit}, {base}, {w};")
+            else:
+                hit = base
+            self.remember(key, hit)
+        return hit, flat.const * self.esz
+
+
+# ---------------------------------------------------------------------------
+# expression emission
+# ---------------------------------------------------------------------------
+
+
+class Expr:
+    """Emit a scalar expression; `read(buf, index_affs, guard)` yields a register."""
+
+    def __init__(self, g: Ptx, iv, read):
+        self.g, self.iv, self.read = g, iv, read
+        self.guard = None           # predicate register: loads run only where it holds
+
+    def lin(self, lin) -> Aff:
+        a = Aff.k(lin.const)
+        for n, c in lin.terms:
+            a = a + self.iv(n).scale(c)
+        return a
+
+    def __call__(self, e) -> str:
+        g = self.g
+        k = kind(e)
+        if k == "Const":
+            return g.fconst(e.value)
+        if k == "IterVal":
+            r = g.aff(self.lin(e.lin))
+            f = g.new(g.fr)
+            g(f"cvt.rn.{g.ft}.s32 {f}, {r};")
+            return f
+        if k == "Read":
+            return self.read(e.buffer, [self.lin(l) for l in e.index], self.guard)
+        if k == "Bin":
+            a, b = self(e.lhs), self(e.rhs)
+            f = g.new(g.fr)
+            op = e.op
+            if op in ("add", "sub", "mul"):
+                g(f"{op}.rn.{g.ft} {f}, {a}, {b};" if op != "sub" else f"sub.rn.{g.ft} {f}, {a}, {b};")
+            elif op == "div":
+                g(f"div.rn.{g.ft} {f}, {a}, {b};")
+            elif op in ("max", "min"):
+                g(f"{op}.{g.ft} {f}, {a}, {b};")
+            else:
+                p = g.new("%p")
+                g(f"setp.{op}.{g.ft} {p}, {a}, {b};")
+                g(f"selp.{g.ft} {f}, {g.fconst(1.0)}, {g.fconst(0.0)}, {p};")
+            return f
+        if k == "Call":
+            a = self(e.arg)
+            f = g.new(g.fr)
+            if e.fn == "sqrt":
+                g(f"sqrt.rn.{g.ft} {f}, {a};")
+            elif e.fn == "abs":
+                g(f"abs.{g.ft} {f}, {a};")
+            else:
+                raise Unsupported(f"math call {e.fn}")
+            return f
+        if k == "Select":
+            c = self(e.cond)
+            p = g.new("%p")
+            g(f"setp.ne.{g.ft} {p}, {c}, {g.fconst(0.0)};")
+            np_ = g.new("%p")
+            g(f"not.pred {np_}, {p};")
+            outer = self.guard
+            pt, pf = p, np_
+            if outer is not None:
+                pt, pf = g.new("%p"), g.new("%p")
+                g(f"and.pred {pt}, {p}, {outer};")
+                g(f"and.pred {pf}, {np_}, {outer};")
+            self.guard = pt
+            t = self(e.then)
+            self.guard = pf
+            o = self(e.other)
+            self.guard = outer
+            f = g.new(g.fr)
+            g(f"selp.{g.ft} {f}, {t}, {o}, {p};")
+            return f
+        raise Unsupported(f"expression node {k}")
+
+
+# ---------------------------------------------------------------------------
+# kernel emission
+# ---------------------------------------------------------------------------
+
+
+class _Mod:
+    """Module-level state shared by the kernels of one candidate."""
+
+    def __init__(self, p, dtype):
+        self.p, self.dtype, self.dag = p, dtype, p.dag
+        self.live = {s.name: s for s in p.stages if not s.inlined}
+        self.layouts = dict(p.layouts)
+        self.buffers: dict = {}
+
+    def shape(self, name):
+        if name in self.live:
+            return tuple(e for _, e in self.live[name].space)
+        return self.dag.node(name).shape
+
+
+class _Kern:
+    def __init__(self, mod: _Mod, entry: str, threads: int):
+        self.m = mod
+        self.g = Ptx(mod.dtype)
+        self.entry = entry
+        self.threads = threads
+        self.params: list = []          # buffer names in order
+        self.ptr: dict = {}             # buffer -> 64-bit global pointer register
+        self.writes: set = set()
+        self.body: list = []
+
+    def param(self, name: str) -> str:
+        if name not in self.ptr:
+            self.params.append(name)
+            self.ptr[name] = f"%ptr{len(self.params)}"
+        return self.ptr[name]
+
+    # -- global memory ----------------------------------------------------
+    def gflat(self, name: str, idx: list) -> Aff:
+        shape = self.m.shape(name)
+        flat, mul = Aff.k(0), 1
+        for d in range(len(shape) - 1, -1, -1):
+            flat = flat + idx[d].scale(mul)
+            mul *= shape[d]
+        return flat
+
+    def gload(self, name: str, idx: list, guard) -> str:
+        g, m = self.g, self.m
+        desc = m.layouts.get(name) if name not in m.live else None
+        if desc is not None:
+            key = f"{name}#packed"
+            if key not in m.buffers:
+                m.buffers[key] = Buffer(key, tuple(e for _, e in desc), "packed", tuple(desc), name)
+            base = self.param(key)
+            regs = {}
+            flat, mul = Aff.k(0), 1
+            for j in range(len(desc) - 1, -1, -1):
+                d, e = desc[j]
+                st = 1
+                for d2, e2 in desc[j + 1:]:
+                    if d2 == d:
+                        st *= e2
+                if d not in regs:
+                    regs[d] = g.aff(idx[d])
+                x = g.udiv(regs[d], st)
+                if e < m.shape(name)[d] or st > 1:
+                    x = g.urem(x, e)
+                flat = flat + Aff.reg(x, mul)
+                mul *= e
+        else:
+            if name not in m.live and name not in m.buffers:
+                m.buffers[name] = Buffer(name, m.shape(name), "input")
+            base = self.param(name)
+            flat = self.gflat(name, idx)
+        key = ("gld", base, flat.key(), flat.const, guard)
+        hit = g.cached(key)
+        if hit:
+            return hit
+        rb, imm = g.gaddr(base, flat)
+        f = g.new(g.fr)
+        pred = f"@{guard} " if guard else ""
+        if guard:
+            g(f"mov.b{32 if g.ft == 'f32' else 64} {f}, 0;")
+        g(f"{pred}ld.global.nc.{g.ft} {f}, [{rb}+{imm}];")
+        return g.remember(key, f)
+
+    def gstore(self, name: str, idx: list, val: str) -> None:
+        g = self.g
+        base = self.param(name)
+        self.writes.add(name)
+        rb, imm = g.gaddr(base, self.gflat(name, idx))
+        g(f"st.global.{g.ft} [{rb}+{imm}], {val};")
+
+    # -- inline producers and readers ---------------------------------------
+    def reader(self, stage, iv, override=None):
+        attached_prod = {s.name for s in _attached(self.m.p, stage.name) if _reads_buffer(stage.expr, s.name)}
+
+        def read(buf, idx, guard):
+            if override is not None:
+                r = override(buf, idx, guard)
+                if r is not None:
+                    return r
+            if buf in attached_prod:
+                return self.producer(buf, idx, guard)
+            return self.gload(buf, idx, guard)
+        return read
+
+    def producer(self, name: str, idx: list, guard) -> str:
+        g = self.g
+        s = self.m.live[name]
+        env = {n: a for (n, _), a in zip(s.space, idx)}
+        body = s.expr.body if kind(s.expr) == "Reduce" else s.expr
+        if not s.reduce:
+            ex = Expr(g, lambda n: env[n], self.reader(s, lambda n: env[n]))
+            ex.guard = guard
+            return ex(body)
+        # reducing producer: serial loops, fully unrolled when small
+        op = s.expr.op
+        acc = g.new(g.fr)
+        g(f"mov.{'b32' if g.ft == 'f32' else 'b64'} {acc}, {g.fconst(0.0 if op == 'sum' else -math.inf)};")
+        red = list(s.reduce)
+
+        def rec(i, env):
+            nonlocal acc
+            if i == len(red):
+                ex = Expr(g, lambda n: env[n], self.reader(s, lambda n: env[n]))
+                ex.guard = guard
+                v = ex(body)
+                na = g.new(g.fr)
+                g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {na}, {acc}, {v};")
+                g(f"mov.{'b32' if g.ft == 'f32' else 'b64'} {acc}, {na};")
+                return
+            n, e = red[i]
+            self.loop(e, False, lambda r: rec(i + 1, {**env, n: r}))
+        rec(0, env)
+        return acc
+
+    # -- loops ----------------------------------------------------------------
+    def loop(self, extent: int, unroll: bool, body) -> None:
+        """Counted loop: unrolled -> body(Aff.k(i)) per i; else a PTX loop."""
+        g = self.g
+        if extent == 1:
+            body(Aff.k(0))
+            return
+        if unroll:
+            for i in range(extent):
+                body(Aff.k(i))
+            return
+        v = g.new("%r")
+        lab = g.new_label()
+        g(f"mov.s32 {v}, 0;")
+        g.label(lab)
+        g(".pragma \"nounroll\";")
+        g.push()
+        body(Aff.reg(v))
+        g.pop()
+        p = g.new("%p")
+        g(f"add.s32 {v}, {v}, 1;")
+        g(f"setp.lt.s32 {p}, {v}, {extent};")
+        g(f"@{p} bra {lab};")
+
+    # -- epilogue -------------------------------------------------------------
+    def epilogue(self, host, idx_of: dict, value: str, materialize: bool) -> None:
+        g = self.g
+        space = [n for n, _ in host.space]
+        if materialize:
+            self.gstore(host.name, [idx_of[n] for n in space], value)
+        for c in _attached(self.m.p, host.name):
+            if not _reads_buffer(c.expr, host.name) or _reads_buffer(host.expr, c.name):
+                continue
+            cspace = [n for n, _ in c.space]
+            if len(cspace) != len(space) or c.reduce:
+                raise LoweringError(f"consumer {c.name} cannot be fused")
+            cenv = {cn: idx_of[hn] for cn, hn in zip(cspace, space)}
+
+            def ov(buf, idx, guard, host=host, cspace=cspace):
+                if buf == host.name:
+                    want = [cenv[n] for n in cspace]
+                    if all(a.key() == b.key() and a.const == b.const for a, b in zip(idx, want)):
+                        return value
+                    raise LoweringError(f"consumer {c.name} reads {host.name} at a non-identity index")
+                return None
+            ex = Expr(g, lambda n: cenv[n], self.reader(c, lambda n: cenv[n], override=ov))
+            v = ex(c.expr)
+            self.epilogue(c, {n: cenv[n] for n in cspace}, v, True)
+
+    def text(self) -> str:
+        g = self.g
+        ps = ", ".join(f".param .u64 p{i}" for i in range(len(self.params)))
+        head = [f".visible .entry {self.entry}({ps}) .maxntid {self.threads}, 1, 1", "{"]
+        decl = [f"  .reg .b32 %r<{g.n['%r'] + 1}>;", f"  .reg .b64 %rd<{g.n['%rd'] + 1}>;",
+                f"  .reg .pred %p<{g.n['%p'] + 1}>;",
+                f"  .reg .{g.ft} {g.fr}<{g.n[g.fr] + 1}>;",
+                f"  .reg .b64 %ptr<{len(self.params) + 1}>;"]
+        loads = []
+        for i, _ in enumerate(self.params):
+            loads.append(f"  ld.param.u64 %ptr{i + 1}, [p{i}];")
+            loads.append(f"  cvta.to.global.u64 %ptr{i + 1}, %ptr{i + 1};")
+        return "\n".join(head + decl + self.body + loads + g.lines + ["  ret;", "}"]) + "\n"
+
+
+def _naive(mod: _Mod, s, entry: str) -> tuple:
+    k = _Kern(mod, entry, NAIVE_THREADS)
+    g = k.g
+    sp_loops = [l for l in s.loops if l.kind == "space"]
+    rd_loops = [l for l in s.loops if l.kind != "space"]
+    total = 1
+    for l in sp_loops:
+        total *= l.extent
+    if total >= (1 << 31):
+        raise Unsupported("index space exceeds 2^31")
+    grid = max(1, min((total + NAIVE_THREADS - 1) // NAIVE_THREADS, 148 * 16))
+    dmap = dict(s.index_map)
+    space_names = [n for n, _ in s.space]
+    tid, cta, pidx = g.new("%r"), g.new("%r"), g.new("%r")
+    g(f"mov.u32 {tid}, %tid.x;")
+    g(f"mov.u32 {cta}, %ctaid.x;")
+    g(f"mad.lo.s32 {pidx}, {cta}, {NAIVE_THREADS}, {tid};")
+    top, done = g.new_label(), g.new_label()
+    pe = g.new("%p")
+    g(f"setp.ge.s32 {pe}, {pidx}, {total};")
+    g(f"@{pe} bra {done};")
+    g.label(top)
+    g.push()
+    lv = {}
+    digits = g.decompose(pidx, [l.extent for l in sp_loops]) if sp_loops else []
+    for l, d in zip(sp_loops, digits):
+        lv[l.id] = Aff.reg(d)
+
+    def dec(d, lv):
+        kk = kind(d)
+        if kk == "DVar":
+            return lv[d.loop]
+        if kk == "DConst":
+            return Aff.k(d.value)
+        if kk == "DAdd":
+            return dec(d.a, lv) + dec(d.b, lv)
+        a = dec(d.a, lv)
+        if kk == "DMul":
+            return a.scale(d.c)
+        r = g.aff(a)
+        return Aff.reg(g.udiv(r, d.c) if kk == "DDiv" else g.urem(r, d.c))
+
+    env = {n: dec(dmap[n], lv) for n in space_names if n in dmap}
+    if rd_loops:
+        op = s.expr.op
+        flags = _unroll_flags([l.extent for l in rd_loops], s.pragma_unroll)
+        acc = g.new(g.fr)
+        mv = "b32" if g.ft == "f32" else "b64"
+        g(f"mov.{mv} {acc}, {g.fconst(0.0 if op == 'sum' else -math.inf)};")
+        body = s.expr.body
+
+        def rec(i, lv):
+            if i == len(rd_loops):
+                env2 = dict(env)
+                for n, d in s.index_map:
+                    if n not in space_names:
+                        env2[n] = dec(d, lv)
+                ex = Expr(g, lambda n: env2[n], k.reader(s, lambda n: env2[n]))
+                if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                    a, b = ex(body.lhs), ex(body.rhs)
+                    g(f"fma.rn.{g.ft} {acc}, {a}, {b}, {acc};")
+                else:
+                    v = ex(body)
+                    g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {acc}, {acc}, {v};")
+                return
+            l = rd_loops[i]
+            k.loop(l.extent, flags[i], lambda r: rec(i + 1, {**lv, l.id: r}))
+        rec(0, lv)
+        value = acc
+    else:
+        expr = s.expr.body if kind(s.expr) == "Reduce" else s.expr
+        value = Expr(g, lambda n: env[n], k.reader(s, lambda n: env[n]))(expr)
+    k.epilogue(s, {n: env[n] for n in space_names}, value, _must_materialize(mod, s))
+    g.pop()
+    g(f"add.s32 {pidx}, {pidx}, {grid * NAIVE_THREADS};")
+    g(f"setp.lt.s32 {pe}, {pidx}, {total};")
+    g(f"@{pe} bra {top};")
+    g.label(done)
+    args = _args(k, mod, s)
+    return k, Kernel(entry, grid, NAIVE_THREADS, 0, args, {"template": "naive", "stage": s.name, "points": total})
+
+
+def _args(k: _Kern, mod: _Mod, s) -> list:
+    return list(k.params)
+
+
+def _smem_strides(hull: list, lane_coords) -> tuple:
+    """Row-major strides of a staged tile with the innermost dim padded to
+    minimise shared-memory bank conflicts for the warp's first access."""
+    best = None
+    for pad in range(0, 9):
+        dims = hull[:-1] + [hull[-1] + pad]
+        st, m = [], 1
+        for h in reversed(dims):
+            st.append(m)
+            m *= h
+        st.reverse()
+        banks: dict = {}
+        for coords in lane_coords:
+            addr = sum(c * s for c, s in zip(coords, st))
+            banks.setdefault(addr % 32, set()).add(addr)
+        deg = max(len(v) for v in banks.values()) if banks else 1
+        cand = (deg, m, pad)
+        if best is None or cand < best[0]:
+            best = (cand, st, m)
+        if deg == 1:
+            break
+    return best[1], best[2]
+
+
+def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
+    structure, factors = levels
+    space = [n for n, _ in s.space]
+    red = [n for n, _ in s.reduce]
+    block, vthread, thread, stage_lv, inner = _binding(structure)
+    if not stage_lv:
+        raise LoweringError("tiled stage has no reduction level to stage")
+
+    def f(a, lv):
+        return factors[a][lv[1]]
+
+    def axes_of(lv):
+        return space if lv[0] == "S" else red
+
+    n_threads = n_blocks = n_vt = 1
+    for a in space:
+        for lv in thread:
+            n_threads *= f(a, lv)
+        for lv in block:
+            n_blocks *= f(a, lv)
+        for lv in vthread:
+            n_vt *= f(a, lv)
+    if n_threads > MAX_THREADS:
+        raise LoweringError(f"{n_threads} threads per block exceed {MAX_THREADS}")
+    if n_vt > MAX_VTHREAD:
+        raise LoweringError(f"{n_vt} virtual threads exceed {MAX_VTHREAD}")
+    reg_levels = vthread + [lv for lv in inner if lv[0] == "S"]
+    acc_dims = []
+    for a in space:
+        n = 1
+        for lv in reg_levels:
+            n *= f(a, lv)
+        acc_dims.append(n)
+    n_acc = 1
+    for n in acc_dims:
+        n_acc *= n
+    if n_acc > MAX_ACC:
+        raise LoweringError(f"register tile of {n_acc} accumulators per thread exceeds {MAX_ACC}")
+    n_s, n_r = structure.count("S"), structure.count("R")
+    T = {}
+    for a in space:
+        t = 1
+        for k_ in range(1, n_s):
+            t *= factors[a][k_]
+        T[a] = t
+    RT = {}
+    for r in red:
+        t = 1
+        for k_ in range(1, n_r):
+            t *= factors[r][k_]
+        RT[r] = t
+
+    k = _Kern(mod, entry, n_threads)
+    g = k.g
+    tid, cta = g.new("%r"), g.new("%r")
+    g(f"mov.u32 {tid}, %tid.x;")
+    g(f"mov.u32 {cta}, %ctaid.x;")
+    dig: dict = {}                    # (axis, level tag) -> Aff
+    blk = [(a, lv) for a in space for lv in block if f(a, lv) > 1]
+    for (a, lv), d in zip(blk, g.decompose(cta, [f(a, lv) for a, lv in blk]) if blk else []):
+        dig[(a, lv)] = Aff.reg(d)
+    thr = [(a, lv) for a in space for lv in thread if f(a, lv) > 1]
+    thr_regs = g.decompose(tid, [f(a, lv) for a, lv in thr]) if thr else []
+    for (a, lv), d in zip(thr, thr_regs):
+        dig[(a, lv)] = Aff.reg(d)
+
+    def digit(a, lv):
+        return dig.get((a, lv), Aff.k(0))
+
+    def mixed(a, kind_, lo, dg):
+        n_lv = n_s if kind_ == "S" else n_r
+        e = Aff.k(0)
+        for kk in range(lo, n_lv):
+            e = e.scale(factors[a][kk]) + dg(a, (kind_, kk))
+        return e
+
+    # operands: distinct reads of the reduction body, staged per R0 step
+    body = s.expr.body
+    operands = []
+    for r in reads(body):
+        key = (r.buffer, tuple((l.terms, l.const) for l in r.index))
+        if key not in [o["key"] for o in operands]:
+            operands.append({"key": key, "read": r})
+    attached_prod = {c.name for c in _attached(mod.p, s.name) if _reads_buffer(s.expr, c.name)}
+    span = {**T, **RT}
+    for o in operands:
+        hull, off = [], []
+        for lin in o["read"].index:
+            h, of = 1, 0
+            for n, c in lin.terms:
+                if n not in span:
+                    raise LoweringError(f"read index uses iterator {n} outside the stage")
+                h += abs(c) * (span[n] - 1)
+                if c < 0:
+                    of += -c * (span[n] - 1)
+            hull.append(h)
+            off.append(of)
+        o["hull"], o["off"] = hull, off
+        size = 1
+        for h in hull:
+            size *= h
+        o["size"] = size
+
+    # loop list of the per-thread nest
+    loop_list = []
+    for lv in vthread:
+        for a in space:
+            if f(a, lv) > 1:
+                loop_list.append((a, lv, f(a, lv), True))
+    for lv in inner:
+        for a in axes_of(lv):
+            if f(a, lv) > 1:
+                loop_list.append((a, lv, f(a, lv), False))
+    free = [x for x in loop_list if not x[3]]
+    flags = _unroll_flags([x[2] for x in free], s.pragma_unroll)
+    it = iter(flags)
+    unroll = [True if x[3] else next(it) for x in loop_list]
+    unrolled = 1
+    for x, u in zip(loop_list, unroll):
+        if u:
+            unrolled *= x[2]
+    if unrolled > MAX_UNROLLED:
+        raise LoweringError(f"unrolled body of {unrolled} statements exceeds {MAX_UNROLLED}")
+    acc_in_regs = all(unroll)
+
+    # smem layout: pad each operand's innermost dim against the warp's bank pattern
+    lanes = min(32, n_threads)
+    lane_digits = []
+    for ln in range(lanes):
+        x, dd = ln, {}
+        for (a, lv) in reversed(thr):
+            dd[(a, lv)] = x % f(a, lv)
+            x //= f(a, lv)
+        lane_digits.append(dd)
+    plain = sum(o["size"] for o in operands) * g.esz
+    if plain > MAX_SMEM:
+        raise LoweringError(f"shared memory {plain} bytes exceeds {MAX_SMEM}")
+    total_words = 0
+    for o in operands:
+        coords = []
+        for dd in lane_digits:
+            c = []
+            for di, lin in enumerate(o["read"].index):
+                v = o["off"][di]
+                for n, cc in lin.terms:
+                    if n in T:
+                        loc = 0
+                        for kk in range(1, n_s):
+                            loc = loc * factors[n][kk] + dd.get((n, ("S", kk)), 0)
+                        v += cc * loc
+                c.append(v)
+            coords.append(c)
+        o["stride"], o["words"] = _smem_strides(o["hull"], coords)
+        o["base_word"] = total_words
+        total_words += o["words"]
+    if total_words * g.esz > MAX_SMEM:          # padding must not change legality: drop it
+        total_words = 0
+        for o in operands:
+            st, m = [], 1
+            for h in reversed(o["hull"]):
+                st.append(m)
+                m *= h
+            o["stride"], o["words"], o["base_word"] = st[::-1], m, total_words
+            total_words += m
+    smem_bytes = total_words * g.esz
+    sm = g.new("%r")
+    g(f"mov.u32 {sm}, smem_;")
+
+    # accumulators
+    op = s.expr.op
+    init = g.fconst(0.0 if op == "sum" else -math.inf)
+    mv = "b32" if g.ft == "f32" else "b64"
+    if acc_in_regs:
+        acc = [g.new(g.fr) for _ in range(n_acc)]
+        for r in acc:
+            g(f"mov.{mv} {r}, {init};")
+    else:
+        k.body.append(f"  .local .align 8 .b8 accl[{n_acc * g.esz}];")
+        ab = g.new("%rd")
+        g(f"mov.u64 {ab}, accl;")
+        iv0 = g.new("%r")
+        g(f"mov.s32 {iv0}, 0;")
+        lab = g.new_label()
+        g.label(lab)
+        w = g.new("%rd")
+        g(f"mul.wide.s32 {w}, {iv0}, {g.esz};")
+        a2 = g.new("%rd")
+        g(f"add.s64 {a2}, {ab}, {w};")
+        g(f"st.local.{g.ft} [{a2}], {init};")
+        pz = g.new("%p")
+        g(f"add.s32 {iv0}, {iv0}, 1;")
+        g(f"setp.lt.s32 {pz}, {iv0}, {n_acc};")
+        g(f"@{pz} bra {lab};")
+
+    def acc_index(dg):
+        idx = Aff.k(0)
+        for ai, a in enumerate(space):
+            e = Aff.k(0)
+            for lv in reg_levels:
+                if f(a, lv) > 1:
+                    e = e.scale(f(a, lv)) + dg(a, lv)
+            idx = idx.scale(acc_dims[ai]) + e
+        return idx
+
+    stage_axes = [(r, f(r, stage_lv[0])) for r in red if f(r, stage_lv[0]) > 1]
+
+    def fetch(sdig):
+        for o in operands:
+            r = o["read"]
+            hull = o["hull"]
+            base = []
+            for di, lin in enumerate(r.index):
+                b = Aff.k(lin.const)
+                for n, c in lin.terms:
+                    if n in T:
+                        mn = digit(n, ("S", 0)).scale(T[n])
+                    else:
+                        mn = sdig(n).scale(RT[n])
+                    b = b + (mn.scale(c) if c >= 0 else (mn + (span[n] - 1)).scale(c))
+                base.append(b)
+            trips = -(-o["size"] // n_threads)
+            full = o["size"] % n_threads == 0
+
+            def elem(e_aff, guard_tail):
+                g.push()
+                er = g.aff(e_aff)
+                pt = None
+                if guard_tail:
+                    pt = g.new("%p")
+                    g(f"setp.lt.s32 {pt}, {er}, {o['size']};")
+                cs = g.decompose(er, hull)
+                idx = [b + Aff.reg(c) for b, c in zip(base, cs)]
+                if r.buffer in attached_prod:
+                    v = k.producer(r.buffer, idx, pt)
+                else:
+                    v = k.gload(r.buffer, idx, pt)
+                saddr = Aff.k(0)
+                for c, st_ in zip(cs, o["stride"]):
+                    saddr = saddr + Aff.reg(c, st_)
+                sa = g.aff(saddr)
+                a = g.new("%r")
+                g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {sm};")
+                pred = f"@{pt} " if pt else ""
+                g(f"{pred}st.shared.{g.ft} [{a}+{o['base_word'] * g.esz}], {v};")
+                g.pop()
+            if trips <= 16:
+                for t in range(trips):
+                    elem(Aff.reg(tid) + t * n_threads, not full and t == trips - 1)
+            else:
+                k.loop(trips, False, lambda tv: elem(Aff.reg(tid) + tv.scale(n_threads), not full))
+
+    def compute(sdig):
+        # per-thread nest; body accumulates into acc
+        glob_loc = {}
+
+        def rec(i, dg):
+            if i == len(loop_list):
+                def dgf(a, lv):
+                    return dg.get((a, lv), digit(a, lv))
+                loc = {a: mixed(a, "S", 1, dgf) for a in space}
+                loc.update({r: mixed(r, "R", 1, dgf) for r in red})
+
+                def sread(buf, idx, guard, dgf=dgf, loc=loc):
+                    raise AssertionError("unreachable")
+
+                def smem(buf, index):
+                    key = (buf, tuple((l.terms, l.const) for l in index))
+                    o = next(o for o in operands if o["key"] == key)
+                    addr = Aff.k(0)
+                    for di, lin in enumerate(index):
+                        c = Aff.k(o["off"][di])
+                        for n, cc in lin.terms:
+                            c = c + loc[n].scale(cc)
+                        addr = addr + c.scale(o["stride"][di])
+                    rt = addr.runtime()
+                    ck = ("sld", o["base_word"], rt.key(), addr.const)
+                    hit = g.cached(ck)
+                    if hit:
+                        return hit
+                    bk = ("sbase", o["base_word"], rt.key())
+                    b = g.cached(bk)
+                    if b is None:
+                        x = g.aff(rt) if rt.terms else None
+                        b = g.new("%r")
+                        if x is None:
+                            g(f"mov.u32 {b}, {sm};")
+                        else:
+                            g(f"mad.lo.s32 {b}, {x}, {g.esz}, {sm};")
+                        g.remember(bk, b)
+                    v = g.new(g.fr)
+                    g(f"ld.shared.{g.ft} {v}, [{b}+{(o['base_word'] + addr.const) * g.esz}];")
+                    return g.remember(ck, v)
+
+                glob = {a: mixed(a, "S", 0, dgf) for a in space}
+                glob.update({r: mixed(r, "R", 0, lambda a, lv: sdig(a) if lv == stage_lv[0] else dgf(a, lv))
+                             for r in red})
+
+                class SE(Expr):
+                    def __call__(self2, e):
+                        if kind(e) == "Read":
+                            return smem(e.buffer, e.index)
+                        return Expr.__call__(self2, e)
+                ex = SE(g, lambda n: glob[n], None)
+                ai = acc_index(dgf)
+                if acc_in_regs:
+                    tgt = acc[ai.const]
+                    if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                        a_, b_ = ex(body.lhs), ex(body.rhs)
+                        g(f"fma.rn.{g.ft} {tgt}, {a_}, {b_}, {tgt};")
+                    else:
+                        v = ex(body)
+                        g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {tgt}, {tgt}, {v};")
+                else:
+                    rb, imm = _local_addr(g, ab, ai)
+                    cur = g.new(g.fr)
+                    g(f"ld.local.{g.ft} {cur}, [{rb}+{imm}];")
+                    if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                        a_, b_ = ex(body.lhs), ex(body.rhs)
+                        g(f"fma.rn.{g.ft} {cur}, {a_}, {b_}, {cur};")
+                    else:
+                        v = ex(body)
+                        g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {cur}, {cur}, {v};")
+                    g(f"st.local.{g.ft} [{rb}+{imm}], {cur};")
+                return
+            a, lv, ext, _ = loop_list[i]
+            k.loop(ext, unroll[i], lambda r: rec(i + 1, {**dg, (a, lv): r}))
+        g.push()
+        rec(0, {})
+        g.pop()
+
+    def stage_body(sdig):
+        fetch(sdig)
+        g("bar.sync 0;")
+        compute(sdig)
+        g("bar.sync 0;")
+
+    def stage_rec(i, sd):
+        if i == len(stage_axes):
+            stage_body(lambda r: sd.get(r, Aff.k(0)))
+            return
+        r, e = stage_axes[i]
+        k.loop(e, False, lambda v: stage_rec(i + 1, {**sd, r: v}))
+    stage_rec(0, {})
+
+    # epilogue over the register tile
+    reg_loops = [(a, lv, f(a, lv)) for lv in reg_levels for a in space if f(a, lv) > 1]
+
+    def ep(i, dg):
+        if i == len(reg_loops):
+            def dgf(a, lv):
+                return dg.get((a, lv), digit(a, lv))
+            idx_of = {a: mixed(a, "S", 0, dgf) for a in space}
+            ai = acc_index(dgf)
+            if acc_in_regs:
+                val = acc[ai.const]
+            else:
+                rb, imm = _local_addr(g, ab, ai)
+                val = g.new(g.fr)
+                g(f"ld.local.{g.ft} {val}, [{rb}+{imm}];")
+            g.push()
+            k.epilogue(s, idx_of, val, _must_materialize(mod, s))
+            g.pop()
+            return
+        a, lv, ext = reg_loops[i]
+        k.loop(ext, acc_in_regs, lambda r: ep(i + 1, {**dg, (a, lv): r}))
+    ep(0, {})
+
+    info = {"template": "tiled", "stage": s.name, "structure": structure, "threads": n_threads,
+            "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
+            "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx"}
+    return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
+
+
+def _local_addr(g: Ptx, ab: str, ai: Aff) -> tuple:
+    rt = ai.runtime()
+    if not rt.terms:
+        return ab, ai.const * g.esz
+    key = ("laddr", rt.key())
+    hit = g.cached(key)
+    if hit is None:
+        x = g.aff(rt)
+        w = g.new("%rd")
+        g(f"mul.wide.s32 {w}, {x}, {g.esz};")
+        hit = g.new("%rd")
+        g(f"add.s64 {hit}, {ab}, {w};")
+        g.remember(key, hit)
+    return hit, ai.const * g.esz
+
+
+def lower_ptx(p, dtype: str = "float") -> Lowered:
+    """Same contract as `lower.lower`, but `source` is a PTX module."""
+    if not p.is_concrete():
+        raise LoweringError("program has unresolved symbolic extents")
+    mod = _Mod(p, dtype)
+    kernels, texts = [], []
+    for s in p.stages:
+        if s.inlined or s.compute_at is not None:
+            continue
+        for c in _attached(p, s.name):
+            if _attached(p, c.name) and any(_reads_buffer(c.expr, gg.name) for gg in _attached(p, c.name)):
+                raise LoweringError(f"nested producer attachment under {c.name} is not supported")
+        entry = f"k{len(kernels)}_" + ident(s.name)
+        levels = tile_levels(p, s)
+        if levels is not None:
+            kk, kern = _tiled(mod, s, levels, entry)
+        else:
+            kk, kern = _naive(mod, s, entry)
+        kern.info["backend"] = "ptx"
+        kernels.append(kern)
+        texts.append(kk.text())
+    for name, st in mod.live.items():
+        if name not in mod.buffers:
+            mod.buffers[name] = Buffer(name, tuple(e for _, e in st.space),
+                                       "output" if name in p.dag.outputs else "temp")
+    head = ".version 8.7\n.target sm_100a\n.address_size 64\n.extern .shared .align 16 .b8 smem_[];\n"
+    return Lowered(head + "\n".join(texts), kernels, mod.buffers, list(p.dag.outputs),
+                   {"kernels": [k.info for k in kernels], "backend": "ptx"})
