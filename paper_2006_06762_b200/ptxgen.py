@@ -861,72 +861,124 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             else:
                 k.loop(trips, False, lambda tv: elem(Aff.reg(tid) + tv.scale(n_threads), not full))
 
+    # address coefficients: shared-memory word address of operand o as
+    #   const0 + sum over local level digits (axis, level) of coef * digit
+    def mult(n, lv):
+        m = 1
+        for kk in range(lv[1] + 1, n_s if lv[0] == "S" else n_r):
+            m *= factors[n][kk]
+        return m
+    for o in operands:
+        coef, c0 = {}, o["base_word"]
+        for di, lin in enumerate(o["read"].index):
+            c0 += o["stride"][di] * o["off"][di]
+            for n, cc in lin.terms:
+                kind_ = "S" if n in T else "R"
+                for kk in range(1, n_s if kind_ == "S" else n_r):
+                    lv = (kind_, kk)
+                    if f(n, lv) > 1:
+                        coef[(n, lv)] = coef.get((n, lv), 0) + o["stride"][di] * cc * mult(n, lv)
+        o["coef"], o["c0"] = coef, c0
+    op_of = {o["key"]: o for o in operands}
+    acc_coef = {}
+    m_acc = 1
+    for ai in range(len(space) - 1, -1, -1):
+        a = space[ai]
+        mm = m_acc
+        for lv in reversed(reg_levels):
+            if f(a, lv) > 1:
+                acc_coef[(a, lv)] = mm
+                mm *= f(a, lv)
+        m_acc *= acc_dims[ai]
+    thread_digits = {(a, lv): dig[(a, lv)] for (a, lv) in thr}
+
     def compute(sdig):
-        # per-thread nest; body accumulates into acc
-        glob_loc = {}
+        """Per-thread nest for one staging step; accumulates into acc."""
+        g.push()
+        fma_body = op == "sum" and kind(body) == "Bin" and body.op == "mul"
 
-        def rec(i, dg):
+        def sbase(o, rt_items):
+            key = ("sbase", o["base_word"], rt_items)
+            b = g.cached(key)
+            if b is None:
+                terms = {}
+                for (n, lv), reg in rt_items:
+                    c = o["coef"].get((n, lv), 0)
+                    if c:
+                        terms[reg] = terms.get(reg, 0) + c
+                b = g.new("%r")
+                if terms:
+                    x = g.aff(Aff(terms))
+                    g(f"mad.lo.s32 {b}, {x}, {g.esz}, {sm};")
+                else:
+                    g(f"mov.u32 {b}, {sm};")
+                g.remember(key, b)
+            return b
+
+        state = {"cv": {}, "rv": {}, "rt": ()}
+        thread_items = tuple(sorted((k_, next(iter(a_.terms))) for k_, a_ in thread_digits.items()))
+
+        def smem(buf, index):
+            o = op_of[(buf, tuple((l.terms, l.const) for l in index))]
+            const = o["c0"]
+            cf = o["coef"]
+            for kv, val in state["cv"].items():
+                c = cf.get(kv)
+                if c:
+                    const += c * val
+            b = sbase(o, state["rt"])
+            ck = ("sld", b, const)
+            hit = g.cached(ck)
+            if hit:
+                return hit
+            v = g.new(g.fr)
+            g(f"ld.shared.{g.ft} {v}, [{b}+{const * g.esz}];")
+            return g.remember(ck, v)
+
+        def iv(n):      # global iterator value (only IterVal nodes need it)
+            cv, rv = state["cv"], state["rv"]
+
+            def dgf(a, lv):
+                if (a, lv) in cv:
+                    return Aff.k(cv[(a, lv)])
+                if (a, lv) in rv:
+                    return Aff.reg(rv[(a, lv)])
+                if lv == stage_lv[0] and n in RT:
+                    return sdig(a)
+                return digit(a, lv)
+            return mixed(n, "S" if n in T else "R", 0, dgf)
+
+        class SE(Expr):
+            def __call__(self2, e):
+                if kind(e) == "Read":
+                    return smem(e.buffer, e.index)
+                return Expr.__call__(self2, e)
+        ex = SE(g, iv, None)
+
+        def rec(i, cv, rv):
             if i == len(loop_list):
-                def dgf(a, lv):
-                    return dg.get((a, lv), digit(a, lv))
-                loc = {a: mixed(a, "S", 1, dgf) for a in space}
-                loc.update({r: mixed(r, "R", 1, dgf) for r in red})
-
-                def sread(buf, idx, guard, dgf=dgf, loc=loc):
-                    raise AssertionError("unreachable")
-
-                def smem(buf, index):
-                    key = (buf, tuple((l.terms, l.const) for l in index))
-                    o = next(o for o in operands if o["key"] == key)
-                    addr = Aff.k(0)
-                    for di, lin in enumerate(index):
-                        c = Aff.k(o["off"][di])
-                        for n, cc in lin.terms:
-                            c = c + loc[n].scale(cc)
-                        addr = addr + c.scale(o["stride"][di])
-                    rt = addr.runtime()
-                    ck = ("sld", o["base_word"], rt.key(), addr.const)
-                    hit = g.cached(ck)
-                    if hit:
-                        return hit
-                    bk = ("sbase", o["base_word"], rt.key())
-                    b = g.cached(bk)
-                    if b is None:
-                        x = g.aff(rt) if rt.terms else None
-                        b = g.new("%r")
-                        if x is None:
-                            g(f"mov.u32 {b}, {sm};")
-                        else:
-                            g(f"mad.lo.s32 {b}, {x}, {g.esz}, {sm};")
-                        g.remember(bk, b)
-                    v = g.new(g.fr)
-                    g(f"ld.shared.{g.ft} {v}, [{b}+{(o['base_word'] + addr.const) * g.esz}];")
-                    return g.remember(ck, v)
-
-                glob = {a: mixed(a, "S", 0, dgf) for a in space}
-                glob.update({r: mixed(r, "R", 0, lambda a, lv: sdig(a) if lv == stage_lv[0] else dgf(a, lv))
-                             for r in red})
-
-                class SE(Expr):
-                    def __call__(self2, e):
-                        if kind(e) == "Read":
-                            return smem(e.buffer, e.index)
-                        return Expr.__call__(self2, e)
-                ex = SE(g, lambda n: glob[n], None)
-                ai = acc_index(dgf)
                 if acc_in_regs:
-                    tgt = acc[ai.const]
-                    if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                    ai = 0
+                    for kv, val in cv.items():
+                        ai += acc_coef.get(kv, 0) * val
+                    tgt = acc[ai]
+                    if fma_body:
                         a_, b_ = ex(body.lhs), ex(body.rhs)
                         g(f"fma.rn.{g.ft} {tgt}, {a_}, {b_}, {tgt};")
                     else:
                         v = ex(body)
                         g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {tgt}, {tgt}, {v};")
                 else:
+                    ai = Aff.k(0)
+                    for kv, val in cv.items():
+                        ai = ai + acc_coef.get(kv, 0) * val
+                    for kv, reg in rv.items():
+                        if acc_coef.get(kv):
+                            ai = ai + Aff.reg(reg, acc_coef[kv])
                     rb, imm = _local_addr(g, ab, ai)
                     cur = g.new(g.fr)
                     g(f"ld.local.{g.ft} {cur}, [{rb}+{imm}];")
-                    if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                    if fma_body:
                         a_, b_ = ex(body.lhs), ex(body.rhs)
                         g(f"fma.rn.{g.ft} {cur}, {a_}, {b_}, {cur};")
                     else:
@@ -935,9 +987,21 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     g(f"st.local.{g.ft} [{rb}+{imm}], {cur};")
                 return
             a, lv, ext, _ = loop_list[i]
-            k.loop(ext, unroll[i], lambda r: rec(i + 1, {**dg, (a, lv): r}))
-        g.push()
-        rec(0, {})
+            if unroll[i]:
+                for val in range(ext):
+                    cv[(a, lv)] = val
+                    rec(i + 1, cv, rv)
+                del cv[(a, lv)]
+            else:
+                def inner(r, i=i, a=a, lv=lv):
+                    rv2 = {**rv, (a, lv): next(iter(r.terms))}
+                    saved = (state["rv"], state["rt"])
+                    state["rv"], state["rt"] = rv2, tuple(sorted(rv2.items())) + thread_items
+                    rec(i + 1, cv, rv2)
+                    state["rv"], state["rt"] = saved
+                k.loop(ext, False, inner)
+        state["cv"], state["rt"] = {}, thread_items
+        rec(0, state["cv"], {})
         g.pop()
 
     def stage_body(sdig):
