@@ -733,7 +733,9 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             unrolled *= x[2]
     if unrolled > MAX_UNROLLED:
         raise LoweringError(f"unrolled body of {unrolled} statements exceeds {MAX_UNROLLED}")
-    acc_in_regs = all(unroll)
+    # the accumulator tile is indexed only by space-level digits: it stays in
+    # registers whenever those loops are unrolled (rolled reduction loops are fine)
+    acc_in_regs = all(u for x, u in zip(loop_list, unroll) if x[1][0] == "S")
 
     # smem layout: pad each operand's innermost dim against the warp's bank pattern
     lanes = min(32, n_threads)
@@ -816,7 +818,10 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
 
     stage_axes = [(r, f(r, stage_lv[0])) for r in red if f(r, stage_lv[0]) > 1]
 
-    def fetch(sdig):
+    def fetch_load(sdig, pnext=None):
+        """Issue the global loads (and inline producer math) of one staging step;
+        returns (value, shared word address register, predicate) per element."""
+        items = []
         for o in operands:
             r = o["read"]
             hull = o["hull"]
@@ -833,33 +838,40 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             trips = -(-o["size"] // n_threads)
             full = o["size"] % n_threads == 0
 
-            def elem(e_aff, guard_tail):
-                g.push()
+            def elem(e_aff, guard_tail, o=o, r=r, hull=hull, base=base):
                 er = g.aff(e_aff)
-                pt = None
+                pt = pnext
                 if guard_tail:
                     pt = g.new("%p")
                     g(f"setp.lt.s32 {pt}, {er}, {o['size']};")
+                    if pnext is not None:
+                        g(f"and.pred {pt}, {pt}, {pnext};")
                 cs = g.decompose(er, hull)
-                idx = [b + Aff.reg(c) for b, c in zip(base, cs)]
+                idx = [b_ + Aff.reg(c) for b_, c in zip(base, cs)]
                 if r.buffer in attached_prod:
                     v = k.producer(r.buffer, idx, pt)
                 else:
                     v = k.gload(r.buffer, idx, pt)
-                saddr = Aff.k(0)
+                saddr = Aff.k(o["base_word"])
                 for c, st_ in zip(cs, o["stride"]):
                     saddr = saddr + Aff.reg(c, st_)
-                sa = g.aff(saddr)
-                a = g.new("%r")
-                g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {sm};")
-                pred = f"@{pt} " if pt else ""
-                g(f"{pred}st.shared.{g.ft} [{a}+{o['base_word'] * g.esz}], {v};")
-                g.pop()
+                items.append((v, g.aff(saddr), pt))
             if trips <= 16:
                 for t in range(trips):
                     elem(Aff.reg(tid) + t * n_threads, not full and t == trips - 1)
             else:
-                k.loop(trips, False, lambda tv: elem(Aff.reg(tid) + tv.scale(n_threads), not full))
+                def run(tv, o=o, full=full, elem=elem):
+                    elem(Aff.reg(tid) + tv.scale(n_threads), not full)
+                    fetch_store([items.pop()], sm)
+                k.loop(trips, False, run)
+        return items
+
+    def fetch_store(items, buf):
+        for v, sa, pt in items:
+            a = g.new("%r")
+            g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {buf};")
+            pred = f"@{pt} " if pt else ""
+            g(f"{pred}st.shared.{g.ft} [{a}], {v};")
 
     # address coefficients: shared-memory word address of operand o as
     #   const0 + sum over local level digits (axis, level) of coef * digit
@@ -892,13 +904,13 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         m_acc *= acc_dims[ai]
     thread_digits = {(a, lv): dig[(a, lv)] for (a, lv) in thr}
 
-    def compute(sdig):
+    def compute(sdig, smb):
         """Per-thread nest for one staging step; accumulates into acc."""
         g.push()
         fma_body = op == "sum" and kind(body) == "Bin" and body.op == "mul"
 
         def sbase(o, rt_items):
-            key = ("sbase", o["base_word"], rt_items)
+            key = ("sbase", smb, o["base_word"], rt_items)
             b = g.cached(key)
             if b is None:
                 terms = {}
@@ -909,9 +921,9 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 b = g.new("%r")
                 if terms:
                     x = g.aff(Aff(terms))
-                    g(f"mad.lo.s32 {b}, {x}, {g.esz}, {sm};")
+                    g(f"mad.lo.s32 {b}, {x}, {g.esz}, {smb};")
                 else:
-                    g(f"mov.u32 {b}, {sm};")
+                    g(f"mov.u32 {b}, {smb};")
                 g.remember(key, b)
             return b
 
@@ -1004,19 +1016,64 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         rec(0, state["cv"], {})
         g.pop()
 
-    def stage_body(sdig):
-        fetch(sdig)
-        g("bar.sync 0;")
-        compute(sdig)
-        g("bar.sync 0;")
+    n_stage = 1
+    for _, e in stage_axes:
+        n_stage *= e
+    trips_all = [-(-o["size"] // n_threads) for o in operands]
+    double = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
+              and sum(trips_all) <= 48)
+    if not double:
+        def stage_rec(i, sd):
+            if i == len(stage_axes):
+                sdig = lambda r, sd=sd: sd.get(r, Aff.k(0))  # noqa: E731
+                g.push()
+                items = fetch_load(sdig)
+                fetch_store(items, sm)
+                g.pop()
+                g("bar.sync 0;")
+                compute(sdig, sm)
+                g("bar.sync 0;")
+                return
+            r, e = stage_axes[i]
+            k.loop(e, False, lambda v: stage_rec(i + 1, {**sd, r: v}))
+        stage_rec(0, {})
+    else:
+        # software pipeline: the next step's global loads are issued before this
+        # step's FMAs and land in the other shared-memory buffer afterwards
+        buf = total_words * g.esz
+        radices = [e for _, e in stage_axes]
 
-    def stage_rec(i, sd):
-        if i == len(stage_axes):
-            stage_body(lambda r: sd.get(r, Aff.k(0)))
-            return
-        r, e = stage_axes[i]
-        k.loop(e, False, lambda v: stage_rec(i + 1, {**sd, r: v}))
-    stage_rec(0, {})
+        def digits_of(treg):
+            ds = g.decompose(treg, radices)
+            m = {r: Aff.reg(d) for (r, _), d in zip(stage_axes, ds)}
+            return lambda r: m.get(r, Aff.k(0))
+        g.push()
+        fetch_store(fetch_load(lambda r: Aff.k(0)), sm)
+        g.pop()
+        g("bar.sync 0;")
+        t = g.new("%r")
+        lab = g.new_label()
+        g(f"mov.s32 {t}, 0;")
+        g.label(lab)
+        g(".pragma \"nounroll\";")
+        g.push()
+        par, smb, nbuf, t1, pn = g.new("%r"), g.new("%r"), g.new("%r"), g.new("%r"), g.new("%p")
+        g(f"and.b32 {par}, {t}, 1;")
+        g(f"mad.lo.s32 {smb}, {par}, {buf}, {sm};")
+        g(f"xor.b32 {nbuf}, {par}, 1;")
+        g(f"mad.lo.s32 {nbuf}, {nbuf}, {buf}, {sm};")
+        g(f"add.s32 {t1}, {t}, 1;")
+        g(f"setp.lt.s32 {pn}, {t1}, {n_stage};")
+        items = fetch_load(digits_of(t1), pn)
+        compute(digits_of(t), smb)
+        fetch_store(items, nbuf)
+        g("bar.sync 0;")
+        g.pop()
+        g(f"add.s32 {t}, {t}, 1;")
+        pl = g.new("%p")
+        g(f"setp.lt.s32 {pl}, {t}, {n_stage};")
+        g(f"@{pl} bra {lab};")
+        smem_bytes = 2 * buf
 
     # epilogue over the register tile
     reg_loops = [(a, lv, f(a, lv)) for lv in reg_levels for a in space if f(a, lv) > 1]
@@ -1043,7 +1100,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
 
     info = {"template": "tiled", "stage": s.name, "structure": structure, "threads": n_threads,
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
-            "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx"}
+            "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx",
+            "double_buffered": double}
     return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
 
 
