@@ -586,20 +586,21 @@ def _args(k: _Kern, mod: _Mod, s) -> list:
     return list(k.params)
 
 
-def _smem_strides(hull: list, lane_coords) -> tuple:
-    """Row-major strides of a staged tile with the innermost dim padded to
-    minimise shared-memory bank conflicts for the warp's first access."""
+def _smem_strides(hull: list, lane_coords, order=None, step: int = 1) -> tuple:
+    """Strides (indexed by hull dim) of a staged tile laid out in `order`
+    (outer->inner), innermost dim padded by a multiple of `step` to minimise
+    shared-memory bank conflicts of the warp's first access."""
+    order = list(range(len(hull))) if order is None else order
     best = None
-    for pad in range(0, 9):
-        dims = hull[:-1] + [hull[-1] + pad]
-        st, m = [], 1
-        for h in reversed(dims):
-            st.append(m)
-            m *= h
-        st.reverse()
+    for pad in range(0, 9, step):
+        st = [0] * len(hull)
+        m = 1
+        for j, d in enumerate(reversed(order)):
+            st[d] = m
+            m *= hull[d] + (pad if j == 0 else 0)
         banks: dict = {}
         for coords in lane_coords:
-            addr = sum(c * s for c, s in zip(coords, st))
+            addr = sum(c * s_ for c, s_ in zip(coords, st))
             banks.setdefault(addr % 32, set()).add(addr)
         deg = max(len(v) for v in banks.values()) if banks else 1
         cand = (deg, m, pad)
@@ -749,6 +750,22 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     plain = sum(o["size"] for o in operands) * g.esz
     if plain > MAX_SMEM:
         raise LoweringError(f"shared memory {plain} bytes exceeds {MAX_SMEM}")
+    # innermost register level per space axis: unit-stride runs there allow
+    # vector shared loads when that dim is laid out innermost
+    last_s = [lv for lv in reg_levels if lv in inner] or reg_levels
+    for o in operands:
+        o["vec"], o["order"] = 1, list(range(len(o["hull"])))
+        if not last_s:
+            continue
+        lv4 = last_s[-1]
+        for di, lin in enumerate(o["read"].index):
+            for n, cc in lin.terms:
+                if n in T and cc == 1 and f(n, lv4) > 1 and o["off"][di] % 4 == 0 and \
+                        sum(1 for l2 in o["read"].index for n2, _ in l2.terms if n2 == n) == 1:
+                    w = 4 if f(n, lv4) % 4 == 0 else (2 if f(n, lv4) % 2 == 0 else 1)
+                    if w > o["vec"]:
+                        o["vec"], o["vaxis"] = w, n
+                        o["order"] = [d for d in range(len(o["hull"])) if d != di] + [di]
     total_words = 0
     for o in operands:
         coords = []
@@ -764,7 +781,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                         v += cc * loc
                 c.append(v)
             coords.append(c)
-        o["stride"], o["words"] = _smem_strides(o["hull"], coords)
+        o["stride"], o["words"] = _smem_strides(o["hull"], coords, o["order"], o["vec"])
+        total_words = -(-total_words // 4) * 4          # 16-byte aligned operand bases
         o["base_word"] = total_words
         total_words += o["words"]
     if total_words * g.esz > MAX_SMEM:          # padding must not change legality: drop it
@@ -775,7 +793,9 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 st.append(m)
                 m *= h
             o["stride"], o["words"], o["base_word"] = st[::-1], m, total_words
+            o["vec"] = 1
             total_words += m
+    total_words = -(-total_words // 4) * 4
     smem_bytes = total_words * g.esz
     sm = g.new("%r")
     g(f"mov.u32 {sm}, smem_;")
@@ -891,6 +911,13 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     if f(n, lv) > 1:
                         coef[(n, lv)] = coef.get((n, lv), 0) + o["stride"][di] * cc * mult(n, lv)
         o["coef"], o["c0"] = coef, c0
+        w = o["vec"]
+        if w > 1:   # every run must start on a w-word boundary, or fall back to scalar loads
+            lv4 = ([lv for lv in reg_levels if lv in inner] or reg_levels)[-1]
+            ok = c0 % w == 0 and coef.get((o["vaxis"], lv4)) == 1 and f(o["vaxis"], lv4) % w == 0
+            ok = ok and all(c % w == 0 for kv, c in coef.items() if kv != (o["vaxis"], lv4))
+            if not ok:
+                o["vec"] = 1
     op_of = {o["key"]: o for o in operands}
     acc_coef = {}
     m_acc = 1
@@ -943,6 +970,14 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             hit = g.cached(ck)
             if hit:
                 return hit
+            w = o["vec"] if g.ft == "f32" else 1
+            if w > 1:
+                g0 = const - const % w
+                regs = [g.new(g.fr) for _ in range(w)]
+                g(f"ld.shared.v{w}.{g.ft} {{{', '.join(regs)}}}, [{b}+{g0 * g.esz}];")
+                for j, rr in enumerate(regs):
+                    g.remember(("sld", b, g0 + j), rr)
+                return regs[const - g0]
             v = g.new(g.fr)
             g(f"ld.shared.{g.ft} {v}, [{b}+{const * g.esz}];")
             return g.remember(ck, v)
