@@ -30,6 +30,9 @@ from .lower import (
 from .state.expr import kind, reads
 
 
+LOOKAHEAD = 64      # statements between a shared-memory load and its first use
+
+
 class Unsupported(Exception):
     pass
 
@@ -957,14 +960,21 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         state = {"cv": {}, "rv": {}, "rt": ()}
         thread_items = tuple(sorted((k_, next(iter(a_.terms))) for k_, a_ in thread_digits.items()))
 
-        def smem(buf, index):
+        def smem_addr(buf, index, cv):
             o = op_of[(buf, tuple((l.terms, l.const) for l in index))]
             const = o["c0"]
             cf = o["coef"]
-            for kv, val in state["cv"].items():
+            for kv, val in cv.items():
                 c = cf.get(kv)
                 if c:
                     const += c * val
+            return o, const
+
+        def smem(buf, index):
+            o, const = smem_addr(buf, index, state["cv"])
+            return smem_load(o, const)
+
+        def smem_load(o, const):
             b = sbase(o, state["rt"])
             ck = ("sld", b, const)
             hit = g.cached(ck)
@@ -1002,7 +1012,43 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 return Expr.__call__(self2, e)
         ex = SE(g, iv, None)
 
+        fma_reads = fma_body and kind(body.lhs) == "Read" and kind(body.rhs) == "Read"
+
+        def region(i, cv):
+            """Fully unrolled suffix of the nest: emit operand loads LOOKAHEAD
+            statements ahead of their FMAs (software pipelining of the shared loads)."""
+            snaps = []
+
+            def enum(j):
+                if j == len(loop_list):
+                    snaps.append(dict(cv))
+                    return
+                a, lv, ext, _ = loop_list[j]
+                for val in range(ext):
+                    cv[(a, lv)] = val
+                    enum(j + 1)
+                del cv[(a, lv)]
+            enum(i)
+            plan = []
+            for sn in snaps:
+                ai = 0
+                for kv, val in sn.items():
+                    ai += acc_coef.get(kv, 0) * val
+                plan.append((ai, smem_addr(body.lhs.buffer, body.lhs.index, sn),
+                             smem_addr(body.rhs.buffer, body.rhs.index, sn)))
+            nxt = 0
+            for si, (ai, la, lb) in enumerate(plan):
+                while nxt < len(plan) and nxt <= si + LOOKAHEAD:
+                    smem_load(*plan[nxt][1])
+                    smem_load(*plan[nxt][2])
+                    nxt += 1
+                ra, rb = smem_load(*la), smem_load(*lb)
+                g(f"fma.rn.{g.ft} {acc[ai]}, {ra}, {rb}, {acc[ai]};")
+
         def rec(i, cv, rv):
+            if acc_in_regs and fma_reads and all(unroll[i:]):
+                region(i, cv)
+                return
             if i == len(loop_list):
                 if acc_in_regs:
                     ai = 0
