@@ -15,6 +15,12 @@
 Search semantics are untouched: with identical scores the batched evolve makes
 the same draws and returns the same candidates as the reference's (tested in
 tests/test_integrate.py).
+
+Opt-in (`install(loomtune, gpu_sampler=True)`): fresh
+samples go through `make_gpu_sampler`, which keeps drawing with the reference's
+own `sample_program` until the State has a legal, GPU-sane launch (the
+reference's CPU-oriented sampler yields ~2% of those for tiled sketches).  This
+changes the search distribution and is off by default.
 """
 
 from __future__ import annotations
@@ -88,14 +94,37 @@ def make_evolve_batched(ev):
     return evolve_batched
 
 
-def install(loomtune) -> dict:
+def gpu_sane(p, min_threads: int = 32) -> bool:
+    """A State whose lowering is legal and whose tiled kernels use a sane thread block."""
+    from .lower import LoweringError, lower
+    try:
+        lo = lower(p)
+    except LoweringError:
+        return False
+    return all(k.info.get("template") != "tiled" or k.info["threads"] >= min_threads for k in lo.kernels)
+
+
+def make_gpu_sampler(sample_program, tries: int = 64):
+    """Rejection sampling around the reference's `sample_program` (src/annotate.py:346)."""
+
+    def sample(sketch, policy, rng):
+        p = None
+        for _ in range(tries):
+            p = sample_program(sketch, policy, rng)
+            if gpu_sane(p):
+                return p
+        return p
+    return sample
+
+
+def install(loomtune, gpu_sampler: bool = False) -> dict:
     """Rebind the reference's hot-path call sites; returns the originals."""
     import importlib
     sched = importlib.import_module(loomtune.__name__ + ".sched")
     cli = importlib.import_module(loomtune.__name__ + ".cli")
     ev = importlib.import_module(loomtune.__name__ + ".evolve")
     orig = {"measure_batch": sched.measure_batch, "train": sched.train, "evolve": sched.evolve,
-            "cli.measure_batch": cli.measure_batch}
+            "cli.measure_batch": cli.measure_batch, "sample_program": sched.sample_program}
     ref_train = sched.train
 
     def train(records, hyper=None):
@@ -105,6 +134,8 @@ def install(loomtune) -> dict:
     cli.measure_batch = measure_batch
     sched.train = train
     sched.evolve = make_evolve_batched(ev)
+    if gpu_sampler:
+        sched.sample_program = make_gpu_sampler(orig["sample_program"])
     return orig
 
 
@@ -116,3 +147,4 @@ def uninstall(loomtune, orig: dict) -> None:
     sched.train = orig["train"]
     sched.evolve = orig["evolve"]
     cli.measure_batch = orig["cli.measure_batch"]
+    sched.sample_program = orig["sample_program"]

@@ -35,12 +35,13 @@ from paper_2006_06762_b200.state import workloads as W  # noqa: E402
 
 def main() -> None:
     cfg, budget = sys.argv[1], int(sys.argv[2])
-    seed = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    seed = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 0
+    gpu_sampler = "--gpu-sampler" in sys.argv
     name, kw = W.CONFIGS[cfg]
     dag = LT.ComputeDAG.from_json(W.build(name, **kw).to_json())
     runner = measure.configure(device=0, cache_dir="")
     sched = importlib.import_module("loomtune.sched")
-    orig = integrate.install(LT)
+    orig = integrate.install(LT, gpu_sampler=gpu_sampler)
     timers = {"evolve": 0.0, "measure": 0.0, "train": 0.0}
 
     def timed(key, fn):
@@ -67,7 +68,7 @@ def main() -> None:
     wall = time.perf_counter() - t0
     integrate.uninstall(LT, orig)
     best = task.best_cost
-    out = {"config": cfg, "budget": budget, "seed": seed, "wall_s": wall, "timers": timers,
+    out = {"config": cfg, "budget": budget, "seed": seed, "gpu_sampler": gpu_sampler, "wall_s": wall, "timers": timers,
            "measured": len(measured), "valid": sum(m["status"] == "valid" for m in measured),
            "best_us": best, "best_tflops": FLOPS[cfg] / (best * 1e-6) / 1e12,
            "latency_curve": task.latency, "runner": runner.stats,
