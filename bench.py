@@ -231,6 +231,7 @@ def main() -> None:
     torch.cuda.set_device(local)
     from paper_2006_06762_b200 import measure
     from paper_2006_06762_b200 import runtime as rt
+    from paper_2006_06762_b200.dist import measure_batch_sharded as sharded_measure
     from paper_2006_06762_b200.state import replay
 
     workers = max(1, cores // world - (1 if world == 1 else 0))
@@ -244,8 +245,9 @@ def main() -> None:
         raise SystemExit(f"stream has {len(stream)} States, run needs {need}")
 
     def batch(step: int):
-        lo = (step * world + rank) * B
-        return [replay(dag, h) for h in stream[lo:lo + B]]
+        """The whole step's batch (B per rank); each rank measures its own shard."""
+        lo = step * world * B
+        return [replay(dag, h) for h in stream[lo:lo + world * B]]
 
     def sync():
         torch.cuda.synchronize()
@@ -266,7 +268,7 @@ def main() -> None:
                 for c in runner.ctx.values():
                     runner.lib.lt_task_destroy(c.task)
                 runner.ctx.clear()
-            res = measure.measure_batch(ps)
+            res = sharded_measure(ps)          # NCCL all_gather of (status, cost) records
             all_recs.append(res)
             launch_log.append(list(runner.last_records))
         e1.record()
@@ -284,29 +286,29 @@ def main() -> None:
         ms = run_steps(args.warmup, args.steps, False)
     stats = dict(runner.stats)
     timed = all_recs[-args.steps:]
+    io0 = dict(runner.io)
     timed_records = [r for step in launch_log[-args.steps:] for r in step]
     # our kernels launched in the timed region: per measured candidate, its kernels x
     # (warm-up + repeats), plus one NaN-poison and one verification launch per output
     n_launch = sum(len(r.info.get("kernels", [])) * (1 + r.repeats) + 2 * r.n_outputs
                    for r in timed_records if r.repeats)
+    io1 = dict(runner.io)
     e2e_ms = run_steps(args.warmup + args.steps, args.steps, True)
+    io2 = dict(runner.io)
+    h2d_step = (io2["h2d"] - io1["h2d"]) / args.steps
+    d2h_step = (io2["d2h"] - io1["d2h"]) / args.steps
 
-    # gather measured records (status, cost) over NCCL: the only cross-rank exchange
-    flat = [(1.0 if r.status == "valid" else 0.0, r.cost if math.isfinite(r.cost) else -1.0)
-            for rs in timed for r in rs]
-    mine = torch.tensor(flat, dtype=torch.float64, device="cuda")
-    if world > 1:
-        bufs = [torch.empty_like(mine) for _ in range(world)]
-        dist.all_gather(bufs, mine)
-        gathered = torch.cat(bufs).cpu().numpy()
-    else:
-        gathered = mine.cpu().numpy()
-    n_total = len(gathered)
-    n_valid = int(gathered[:, 0].sum())
-    costs = gathered[gathered[:, 0] > 0, 1]
-    best_us = float(costs.min()) if len(costs) else float("nan")
+    # every rank already holds the gathered, input-ordered results of each step
+    n_total = sum(len(rs) for rs in timed)
+    n_valid = sum(r.status == "valid" for rs in timed for r in rs)
+    costs = [r.cost for rs in timed for r in rs if r.status == "valid"]
+    best_us = min(costs) if costs else float("nan")
     value = n_total / (ms / 1000.0)
     e2e = (args.steps * B * world) / (e2e_ms / 1000.0)
+    if world > 1:   # launches of all ranks
+        t = torch.tensor([n_launch], device="cuda")
+        dist.all_reduce(t)
+        n_launch = int(t.item())
 
     if rank == 0:
         lib = rt.load()
@@ -337,8 +339,10 @@ def main() -> None:
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "kernel": "best candidate of the timed steps (cost = mean of CUDA-event repeats)",
                          "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU"},
-            "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
-                    "note": "fresh DAG context per step: inputs H2D + fp64 ground truth inside the region"},
+            "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
+                    "d2h_bytes_per_step": int(d2h_step),
+                    "note": "measure_batch on host Programs with a fresh DAG context per step: input tensors "
+                            "(fp32+fp64) and cubins H2D, fp64 ground truth recomputed, error words D2H"},
             "gpu_launches": n_launch,
         }
         line["clocks"] = clk.summary()

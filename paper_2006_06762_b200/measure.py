@@ -22,6 +22,8 @@ from __future__ import annotations
 import atexit
 import ctypes
 import hashlib
+import queue
+import threading
 import json
 import math
 import os
@@ -143,6 +145,7 @@ class _DagContext:
         sid = self.slot(key, arr.nbytes)
         rt.check(self.r.lib.lt_task_upload(self.task, sid, arr.ctypes.data, arr.nbytes), f"upload {key}")
         self.h2d_bytes += arr.nbytes
+        self.r.io["h2d"] += arr.nbytes
         return sid
 
     def buffer_slot(self, b, fp64: bool) -> int:
@@ -210,8 +213,13 @@ class Runner:
         self.min_ms, self.max_repeat, self.min_repeat = min_ms, max_repeat, min_repeat
         self.backend = backend
         self.ctx: dict = {}
+        self._dag_keys: dict = {}          # (id(dag), seed) -> (dag, content key)
         self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
+        self.mod_lock = threading.Lock()
+        self.failed_keys: dict = {}
+        self._drain_error = None
         self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0}
+        self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
 
     def close(self):
@@ -224,7 +232,11 @@ class Runner:
         self.lib.lt_pool_stop()
 
     def context(self, dag, seed: int) -> _DagContext:
-        key = _dag_key(dag, seed)
+        hit = self._dag_keys.get((id(dag), seed))
+        if hit is None or hit[0] is not dag:
+            hit = (dag, _dag_key(dag, seed))
+            self._dag_keys[(id(dag), seed)] = hit
+        key = hit[1]
         if key not in self.ctx:
             self.ctx[key] = _DagContext(self, dag, seed)
         return self.ctx[key]
@@ -253,10 +265,12 @@ class Runner:
         return st.value, secs.value, bool(hit.value), buf.raw[:n.value]
 
     def load(self, key: str, image: bytes, entries: list) -> list:
-        if key in self.modules:
-            self.modules.move_to_end(key)
-            return self.modules[key][1]
+        with self.mod_lock:
+            if key in self.modules:
+                self.modules.move_to_end(key)
+                return self.modules[key][1]
         m = self.lib.lt_module_load(self.device, image, len(image))
+        self.io["h2d"] += len(image)
         if not m:
             raise rt.NativeError(f"module load: {self.lib.lt_last_error().decode()}")
         funcs = []
@@ -265,10 +279,11 @@ class Runner:
             if not f:
                 raise rt.NativeError(f"function {e}: {self.lib.lt_last_error().decode()}")
             funcs.append(f)
-        self.modules[key] = (m, funcs)
-        while len(self.modules) > 512:
-            _, (old, _) = self.modules.popitem(last=False)
-            self.lib.lt_module_unload(old)
+        with self.mod_lock:
+            self.modules[key] = (m, funcs)
+            while len(self.modules) > 512:
+                _, (old, _) = self.modules.popitem(last=False)
+                self.lib.lt_module_unload(old)
         return funcs
 
     def compile_and_load(self, sources: list, entries: list) -> list:
@@ -282,77 +297,125 @@ class Runner:
                 out.append(self.load(hashlib.sha1(s.encode()).hexdigest(), data, e))
         return out
 
-    def _completion_order(self, pending: list):
-        """Yield pending candidates as their compiles finish (cached ones first)."""
-        ready = [x for x in pending if x[4] is None]
-        waiting = [x for x in pending if x[4] is not None]
-        for x in ready:
-            yield x
-        while waiting:
-            done = None
-            for k, x in enumerate(waiting):
-                if self.lib.lt_compile_ready(x[4]):
-                    done = k
-                    break
-            if done is None:
-                time.sleep(0.002)
-                continue
-            yield waiting.pop(done)
-
     # -- measurement ---------------------------------------------------------
     def measure_programs(self, programs: list, seed: int = 0) -> list:
+        """Validate + lower on this thread while a measurement thread drains
+        finished compiles onto the GPU (ctypes drops the GIL inside lt_measure)."""
         recs = [Record() for _ in programs]
-        pending = []
-        for i, p in enumerate(programs):
-            bad = validate(p)
-            if bad:
-                recs[i].detail = bad[0]
-                continue
-            t0 = time.perf_counter()
-            try:
-                lo = self.lower(p)
-            except LoweringError as e:
-                recs[i].detail = f"gpu: {e}"
-                recs[i].lower_s = time.perf_counter() - t0
-                continue
-            recs[i].lower_s = time.perf_counter() - t0
-            recs[i].info = lo.info
-            key = hashlib.sha1(lo.source.encode()).hexdigest()
-            job = None if key in self.modules else self.submit(lo.source)
-            pending.append((i, p, lo, key, job))
-        # measure in compile-completion order so the GPU overlaps the slowest compiles
-        order = self._completion_order(pending)
-        for i, p, lo, key, job in order:
-            rec = recs[i]
-            if job is None:
-                funcs = self.load(key, b"", [k.entry for k in lo.kernels])
-                rec.cache_hit = True
-            else:
-                st, secs, hit, data = self.collect(job)
-                rec.compile_s, rec.cache_hit = secs, hit
-                self.stats["compile_s"] += secs
-                self.stats["cache_hits" if hit else "compiled"] += 1
-                if st != 0:
-                    rec.detail = "gpu: compile failed: " + data.decode(errors="replace").strip()[:300]
+        for p in programs:                       # device contexts are created up front
+            self.context(p.dag, seed)
+        q: queue.Queue = queue.Queue()
+        worker = threading.Thread(target=self._drain, args=(q, recs, seed), daemon=True)
+        worker.start()
+        batch_keys: dict = {}
+        try:
+            for i, p in enumerate(programs):
+                bad = validate(p)
+                if bad:
+                    recs[i].detail = bad[0]
                     continue
-                funcs = self.load(key, data, [k.entry for k in lo.kernels])
-            ctx = self.context(p.dag, seed)
-            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
-            self.stats["measured"] += 1
-            rec.first_us, rec.repeats = m.first_us, m.repeats
-            rec.n_outputs = len(lo.outputs)
-            rec.max_rel_err = float(m.max_rel_err)
-            if m.status != 0:
-                rec.detail = "gpu: " + m.detail.decode(errors="replace")
-                continue
-            if not (rec.max_rel_err <= GPU_TOL):
-                names = ",".join(lo.outputs)
-                rec.detail = f"output {names} differs from reference (max rel err {rec.max_rel_err:.3g})"
-                continue
-            rec.status = VALID
-            rec.cost_us = m.cost_us
+                t0 = time.perf_counter()
+                try:
+                    lo = self.lower(p)
+                except LoweringError as e:
+                    recs[i].detail = f"gpu: {e}"
+                    recs[i].lower_s = time.perf_counter() - t0
+                    continue
+                recs[i].lower_s = time.perf_counter() - t0
+                recs[i].info = lo.info
+                key = hashlib.sha1(lo.source.encode()).hexdigest()
+                with self.mod_lock:
+                    loaded = key in self.modules
+                if loaded:
+                    job = None
+                elif key in batch_keys:
+                    job = ("dup", key)
+                else:
+                    job = self.submit(lo.source)
+                    batch_keys[key] = job
+                q.put((i, p, lo, key, job))
+        finally:
+            q.put(None)
+            worker.join()
+        if self._drain_error is not None:
+            err, self._drain_error = self._drain_error, None
+            raise err
         self.last_records = recs
         return recs
+
+    def _ready(self, item) -> bool:
+        job = item[4]
+        if job is None:
+            return True
+        if isinstance(job, tuple):
+            with self.mod_lock:
+                return job[1] in self.modules or job[1] in self.failed_keys
+        return self.lib.lt_compile_ready(job) != 0
+
+    def _drain(self, q, recs, seed) -> None:
+        waiting, closed = [], False
+        try:
+            while True:
+                while True:
+                    try:
+                        item = q.get_nowait() if (waiting or closed) else q.get(timeout=0.05)
+                    except queue.Empty:
+                        break
+                    if item is None:
+                        closed = True
+                    else:
+                        waiting.append(item)
+                idx = next((k for k, x in enumerate(waiting) if self._ready(x)), None)
+                if idx is None:
+                    if closed and not waiting:
+                        return
+                    time.sleep(0.001)
+                    continue
+                self._measure_one(waiting.pop(idx), recs, seed)
+        except BaseException as e:          # surfaced on the calling thread
+            self._drain_error = e
+            while not closed:
+                if q.get() is None:
+                    closed = True
+
+    def _measure_one(self, item, recs, seed) -> None:
+        i, p, lo, key, job = item
+        rec = recs[i]
+        entries = [k.entry for k in lo.kernels]
+        if job is None or isinstance(job, tuple):
+            with self.mod_lock:
+                if key in self.failed_keys:
+                    rec.detail = self.failed_keys[key]
+                    return
+            funcs = self.load(key, b"", entries)
+            rec.cache_hit = True
+        else:
+            st, secs, hit, data = self.collect(job)
+            rec.compile_s, rec.cache_hit = secs, hit
+            self.stats["compile_s"] += secs
+            self.stats["cache_hits" if hit else "compiled"] += 1
+            if st != 0:
+                rec.detail = "gpu: compile failed: " + data.decode(errors="replace").strip()[:300]
+                with self.mod_lock:
+                    self.failed_keys[key] = rec.detail
+                return
+            funcs = self.load(key, data, entries)
+        ctx = self.context(p.dag, seed)
+        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        self.stats["measured"] += 1
+        self.io["d2h"] += 4                                 # the max-relative-error word
+        rec.first_us, rec.repeats = m.first_us, m.repeats
+        rec.n_outputs = len(lo.outputs)
+        rec.max_rel_err = float(m.max_rel_err)
+        if m.status != 0:
+            rec.detail = "gpu: " + m.detail.decode(errors="replace")
+            return
+        if not (rec.max_rel_err <= GPU_TOL):
+            names = ",".join(lo.outputs)
+            rec.detail = f"output {names} differs from reference (max rel err {rec.max_rel_err:.3g})"
+            return
+        rec.status = VALID
+        rec.cost_us = m.cost_us
 
 
 _RUNNER: Runner | None = None
