@@ -170,9 +170,13 @@ __device__ void annotation_block(const int32_t* nest, int n_nest, int ann, doubl
   b[10] = (double)hits;
 }
 
-// Thread-serial reference path for one statement (used for records beyond the
-// warp kernel's shared-memory limits).
-__device__ __noinline__ void row_thread(const int32_t* __restrict__ r, double* __restrict__ out, int* __restrict__ err) {
+__global__ void __launch_bounds__(128)
+features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off,
+                int64_t n_stmt, double* __restrict__ rows, int* __restrict__ err) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_stmt) return;
+  const int32_t* r = words + stmt_off[s];
+  double* out = rows + s * NF;
 
   const int n_nest = r[0], own_start = r[1], n_loops = r[2], n_iter = r[3], n_views = r[4];
   const int unroll = r[5], n_live = r[6], has_reduce = r[7];
@@ -403,370 +407,14 @@ __device__ __noinline__ void row_thread(const int32_t* __restrict__ r, double* _
   }
 }
 
-
-// ---------------------------------------------------------------------------
-// Warp-cooperative kernel: one warp per statement.
-//   phase A  lanes over (range config, iterator): decode-AST intervals with a
-//            register-only stack; plus the two point evaluations for strides
-//   phase B  lanes over (config, view): hull-width products (config 0 also
-//            yields unique lines and the present-loop mask)
-//   phase C  lanes over views: reuse / counter / distance / stride; lanes over
-//            nest positions: working sets
-//   phase D  lane 0 assembles the row in the reference's order into shared
-//            memory; all lanes apply log2(1+x) and store it coalesced.
-// ---------------------------------------------------------------------------
-constexpr int W_REC = 1024, W_CFG = 24, W_IT = 16, W_VIEW = 8, W_DEPTH = 6;
-
-struct WarpSmem {
-  int32_t rec[W_REC];
-  long long ivlo[W_CFG][W_IT], ivhi[W_CFG][W_IT];
-  long long val[2][W_IT];
-  unsigned long long imask[W_IT];
-  long long uprod[W_CFG][W_VIEW];
-  double lines0[W_VIEW];
-  long long last0[W_VIEW];
-  unsigned long long vmask[W_VIEW];
-  short voff[W_VIEW];
-  double tb[W_VIEW], ub[W_VIEW], ul[W_VIEW], cnt[W_VIEW], di[W_VIEW], db[W_VIEW], strd[W_VIEW];
-  int acc[W_VIEW], reuse[W_VIEW];
-  double ws[W_CFG];
-  double row[NF];
-  int bad;
-};
-
-// postfix decode AST over a register stack (interval when point == false)
-__device__ __forceinline__ bool ast_regs(const int32_t* nodes, int cnt, const int32_t* loops, int cfg,
-                                         bool point, int inner, int which, long long& lo, long long& hi) {
-  long long l0 = 0, h0 = 0, l1 = 0, h1 = 0, l2 = 0, h2 = 0, l3 = 0, h3 = 0, l4 = 0, h4 = 0, l5 = 0, h5 = 0;
-  int sp = 0;
-  for (int n = 0; n < cnt; ++n) {
-    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
-    if (op == 0 || op == 1) {
-      long long a, b;
-      if (op == 1) {
-        a = b = arg;
-      } else if (point) {
-        a = b = (arg == inner) ? which : 0;
-      } else {
-        const long long ext = loops[3 * arg];
-        const long long top = (cfg == 0 || loops[3 * arg + 2] > cfg - 1) ? ext - 1 : 0;
-        a = 0;
-        b = top;
-      }
-      if (sp >= W_DEPTH) return false;
-      l5 = l4; h5 = h4; l4 = l3; h4 = h3; l3 = l2; h3 = h2; l2 = l1; h2 = h1; l1 = l0; h1 = h0;
-      l0 = a; h0 = b;
-      ++sp;
-    } else if (op == 2) {
-      if (sp < 2) return false;
-      l0 += l1; h0 += h1;
-      l1 = l2; h1 = h2; l2 = l3; h2 = h3; l3 = l4; h3 = h4; l4 = l5; h4 = h5;
-      --sp;
-    } else {
-      if (sp < 1) return false;
-      const long long c = arg;
-      if (op == 3) {
-        if (c >= 0) { l0 *= c; h0 *= c; } else { long long t = l0; l0 = h0 * c; h0 = t * c; }
-      } else if (op == 4) {
-        l0 = fdiv(l0, c); h0 = fdiv(h0, c);
-      } else if (op == 5) {
-        if (point) { l0 = fmod_(l0, c); h0 = l0; }
-        else if (fdiv(l0, c) == fdiv(h0, c)) { l0 = fmod_(l0, c); h0 = fmod_(h0, c); }
-        else { l0 = 0; h0 = c - 1; }
-      } else {
-        return false;
-      }
-    }
-  }
-  if (sp != 1) return false;
-  lo = l0; hi = h0;
-  return true;
-}
-
-__device__ __forceinline__ long long dim_width_s(const int32_t* d, const long long* lo_t, const long long* hi_t) {
-  long long lo = d[3], hi = d[3];
-  for (int t = 0; t < d[4]; ++t) {
-    const int it = d[5 + 2 * t];
-    const long long c = d[6 + 2 * t];
-    if (c >= 0) { lo += c * lo_t[it]; hi += c * hi_t[it]; }
-    else { lo += c * hi_t[it]; hi += c * lo_t[it]; }
-  }
-  const int st = d[1], pext = d[2];
-  if (pext > 0) {
-    if (st > 1) { lo = fdiv(lo, st); hi = fdiv(hi, st); }
-    if (fdiv(lo, pext) == fdiv(hi, pext)) { lo = fmod_(lo, pext); hi = fmod_(hi, pext); }
-    else { lo = 0; hi = pext - 1; }
-  }
-  const long long size = d[0];
-  lo = lo > 0 ? lo : 0;
-  hi = hi < size - 1 ? hi : size - 1;
-  const long long w = hi - lo + 1;
-  return w > 1 ? w : 1;
-}
-
-__global__ void __launch_bounds__(128)
-features_warp_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off, int64_t n_stmt,
-                     double* __restrict__ rows, int* __restrict__ err) {
-  extern __shared__ __align__(16) unsigned char raw[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  WarpSmem& S = reinterpret_cast<WarpSmem*>(raw)[wib];
-  const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t s = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; s < n_stmt; s += n_warps) {
-    const int64_t off0 = stmt_off[s];
-    const int len = (int)(stmt_off[s + 1] - off0);
-    double* out = rows + s * NF;
-    const int32_t* g = words + off0;
-    const int n_nest = g[0], n_loops = g[2], n_iter = g[3], n_views = g[4];
-    if (len > W_REC || n_nest + 1 > W_CFG || n_iter > W_IT || n_views > W_VIEW || n_loops > 64) {
-      if (lane == 0) row_thread(g, out, err);
-      __syncwarp();
-      continue;
-    }
-    for (int i = lane; i < len; i += 32) S.rec[i] = g[i];
-    if (lane == 0) S.bad = 0;
-    __syncwarp();
-    const int32_t* r = S.rec;
-    const int own_start = r[1], unroll = r[5], n_live = r[6], has_reduce = r[7];
-    const int32_t* ops = r + 8;
-    const int n_nodes = r[17];
-    const int32_t* nest = r + HDR;
-    const int32_t* loops = nest + 4 * n_nest;
-    const int32_t* itab = loops + 3 * n_loops;
-    const int32_t* nodes = itab + 2 * n_iter;
-    const int n_cfg = n_nest + 1;
-    const int inner_own = (n_nest > own_start) ? nest[4 * (n_nest - 1) + 3] : -1;
-    if (lane == 0) {   // view record offsets
-      int o = (int)((nodes + 2 * n_nodes) - r);
-      for (int v = 0; v < n_views; ++v) {
-        S.voff[v] = (short)o;
-        int q = o + 4;
-        for (int k = 0; k < r[o + 3]; ++k) q += 5 + 2 * r[q + 4];
-        o = q;
-      }
-    }
-    // phase A: intervals (cfg, it), point values (which, it), iterator loop masks
-    const int n_a = n_cfg * n_iter + 2 * n_iter + n_iter;
-    for (int w = lane; w < n_a; w += 32) {
-      if (w < n_cfg * n_iter) {
-        const int cfg = w / n_iter, it = w - cfg * n_iter;
-        long long lo, hi;
-        if (!ast_regs(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, cfg, false, -1, 0, lo, hi)) S.bad = 1;
-        S.ivlo[cfg][it] = lo;
-        S.ivhi[cfg][it] = hi;
-      } else if (w < n_cfg * n_iter + 2 * n_iter) {
-        const int q = w - n_cfg * n_iter, which = q / n_iter, it = q - which * n_iter;
-        long long lo = 0, hi = 0;
-        if (inner_own >= 0 &&
-            !ast_regs(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, 0, true, inner_own, which, lo, hi))
-          S.bad = 1;
-        S.val[which][it] = lo;
-      } else {
-        const int it = w - n_cfg * n_iter - 2 * n_iter;
-        unsigned long long m = 0;
-        const int32_t* nd = nodes + 2 * itab[2 * it];
-        for (int n = 0; n < itab[2 * it + 1]; ++n)
-          if (nd[2 * n] == 0) m |= 1ULL << nd[2 * n + 1];
-        S.imask[it] = m;
-      }
-    }
-    __syncwarp();
-    // phase B: (cfg, view) hull products; cfg 0 also unique lines + present mask
-    for (int w = lane; w < n_cfg * n_views; w += 32) {
-      const int cfg = w / n_views, v = w - cfg * n_views;
-      const int32_t* vr = r + S.voff[v];
-      const int nd = vr[3];
-      const int32_t* d = vr + 4;
-      long long prod = 1, last = 1;
-      double lines = 1.0;
-      unsigned long long m = 0;
-      for (int k = 0; k < nd; ++k) {
-        const long long wd = dim_width_s(d, S.ivlo[cfg], S.ivhi[cfg]);
-        prod *= wd;
-        if (k < nd - 1) lines *= (double)wd; else last = wd;
-        for (int t = 0; t < d[4]; ++t) m |= S.imask[d[5 + 2 * t]];
-        d += 5 + 2 * d[4];
-      }
-      S.uprod[cfg][v] = prod;
-      if (cfg == 0) { S.lines0[v] = lines; S.last0[v] = last; S.vmask[v] = m; }
-    }
-    __syncwarp();
-    // phase C: per-view statistics (lanes < n_views) and working sets (lanes over positions)
-    double total = 1.0, red_prod = 1.0;
-    for (int i = 0; i < n_nest; ++i) total *= (double)nest[4 * i];
-    for (int i = own_start; i < n_nest; ++i)
-      if (nest[4 * i + 1] == 1) red_prod *= (double)nest[4 * i];
-    if (lane < n_views) {
-      const int v = lane;
-      const int32_t* vr = r + S.voff[v];
-      const int n_marks = vr[0], hw = vr[1], nd = vr[3];
-      const bool has_w = hw != 0;
-      const bool has_r = (n_marks > hw) || (has_w && red_prod > 1.0);
-      S.acc[v] = (has_w && has_r) ? 2 : (has_w ? 1 : 0);
-      S.ub[v] = (double)S.uprod[0][v] * 4.0;
-      const double lc = ceil((double)(S.last0[v] * 4) / 64.0);
-      S.ul[v] = S.lines0[v] * (lc > 1.0 ? lc : 1.0);
-      S.tb[v] = ((double)n_marks * total) * 4.0;
-      const unsigned long long pm = S.vmask[v];
-      int absent_last = -1;
-      double counter = 1.0;
-      for (int i = 0; i < n_nest; ++i) {
-        const int oi = nest[4 * i + 3];
-        const bool present = oi >= 0 && ((pm >> oi) & 1ULL);
-        if (!present && nest[4 * i] > 1) { counter *= (double)nest[4 * i]; absent_last = i; }
-      }
-      if (has_w && has_reduce && red_prod > 1.0) {
-        S.reuse[v] = 1; S.cnt[v] = red_prod; S.di[v] = 1.0; S.db[v] = (double)(4 * n_marks);
-      } else if (absent_last >= 0) {
-        S.reuse[v] = 0; S.cnt[v] = counter;
-        double dit = 1.0;
-        for (int i = absent_last + 1; i < n_nest; ++i) dit *= (double)nest[4 * i];
-        S.di[v] = dit; S.db[v] = (dit * 4.0) * (double)n_marks;
-      } else {
-        S.reuse[v] = 2; S.cnt[v] = 1.0; S.di[v] = 0.0; S.db[v] = 0.0;
-      }
-      double sd = 0.0;
-      if (inner_own >= 0 && ((pm >> inner_own) & 1ULL)) {
-        long long a0 = 0, a1 = 0, fs = 1;
-        // walk dims inner->outer: collect offsets first
-        int doff[16];
-        const int32_t* d = vr + 4;
-        const int ndd = nd < 16 ? nd : 16;
-        for (int k = 0; k < ndd; ++k) { doff[k] = (int)(d - r); d += 5 + 2 * d[4]; }
-        for (int k = ndd - 1; k >= 0; --k) {
-          const int32_t* dk = r + doff[k];
-          const long long size = dk[0];
-          long long x0 = dk[3], x1 = dk[3];
-          for (int t = 0; t < dk[4]; ++t) {
-            const long long c = dk[6 + 2 * t];
-            x0 += c * S.val[0][dk[5 + 2 * t]];
-            x1 += c * S.val[1][dk[5 + 2 * t]];
-          }
-          if (dk[2] > 0) {
-            if (dk[1] > 1) { x0 = fdiv(x0, dk[1]); x1 = fdiv(x1, dk[1]); }
-            x0 = fmod_(x0, dk[2]); x1 = fmod_(x1, dk[2]);
-          }
-          x0 = x0 < 0 ? 0 : (x0 > size - 1 ? size - 1 : x0);
-          x1 = x1 < 0 ? 0 : (x1 > size - 1 ? size - 1 : x1);
-          a0 += x0 * fs; a1 += x1 * fs;
-          fs *= size;
-        }
-        const long long dlt = a1 - a0;
-        sd = (double)((dlt < 0 ? -dlt : dlt) * 4);
-      }
-      S.strd[v] = sd;
-    }
-    for (int pos = lane; pos < n_nest; pos += 32) {
-      double acc_ws = 0.0;
-      for (int v = 0; v < n_views; ++v) acc_ws += (double)S.uprod[pos + 1][v] * 4.0;
-      S.ws[pos] = acc_ws;
-    }
-    __syncwarp();
-    // phase D: assembly (lane 0), then log2 + coalesced store (all lanes)
-    if (lane == 0) {
-      double* o = S.row;
-      double b[11];
-      for (int k = 0; k < 9; ++k) o[k] = (double)ops[k] * total;
-      for (int k = 9; k < 18; ++k) o[k] = 0.0;
-      annotation_block(nest, n_nest, 2, b);
-      for (int k = 0; k < 11; ++k) o[18 + k] = b[k];
-      for (int k = 0; k < 11; ++k) b[k] = 0.0;
-      long long prod = 1;
-      int n_cov = 0, first = -1, tag = -1;
-      if (unroll > 0 && n_nest > own_start) {
-        for (int i = n_nest - 1; i >= own_start; --i) {
-          if (prod * nest[4 * i] > unroll) break;
-          prod *= nest[4 * i];
-          const int p = position(nest, n_nest, i);
-          tag = (n_cov == 0) ? p : (tag == p ? tag : 7);
-          if (n_cov == 0) first = i;
-          ++n_cov;
-        }
-      }
-      if (!n_cov) b[1] = 1.0;
-      else { b[0] = (double)nest[4 * first]; b[1 + tag] = 1.0; b[9] = (double)prod; b[10] = (double)n_cov; }
-      for (int k = 0; k < 11; ++k) o[29 + k] = b[k];
-      annotation_block(nest, n_nest, 1, b);
-      for (int k = 0; k < 11; ++k) o[40 + k] = b[k];
-      for (int k = 51; k < 59; ++k) o[k] = 0.0;
-      int ops_total = 0;
-      for (int k = 0; k < 9; ++k) ops_total += ops[k];
-      if (n_nest == 0 || ops_total == 0) {
-        for (int k = 59; k < 69; ++k) o[k] = 0.0;
-      } else {
-        double inside[W_CFG + 1];
-        inside[n_nest] = 1.0;
-        for (int i = n_nest - 1; i >= 0; --i) inside[i] = inside[i + 1] * (double)nest[4 * i];
-        for (int j = 1; j <= 10; ++j) {
-          int depth = (int)ceil((double)j / 10.0 * (double)n_nest);
-          if (depth < 1) depth = 1;
-          const int pos = n_nest - depth;
-          double by;
-          if (pos == 0) { by = 0.0; for (int v = 0; v < n_views; ++v) by += S.ub[v]; }
-          else by = S.ws[pos - 1];
-          o[58 + j] = ((double)ops_total * inside[pos]) / (by > 1.0 ? by : 1.0);
-        }
-      }
-      unsigned used = 0;
-      const int n_rank = n_views < 5 ? n_views : 5;
-      for (int slot = 0; slot < 5; ++slot) {
-        double* q = o + 69 + 18 * slot;
-        if (slot >= n_rank) { for (int k = 0; k < 18; ++k) q[k] = 0.0; continue; }
-        int best = -1;
-        for (int v = 0; v < n_views; ++v) {
-          if (used & (1u << v)) continue;
-          const int rk = r[S.voff[v] + 2];
-          if (best < 0 || S.tb[v] > S.tb[best] || (S.tb[v] == S.tb[best] && rk < r[S.voff[best] + 2])) best = v;
-        }
-        used |= 1u << best;
-        const int v = best;
-        for (int k = 0; k < 3; ++k) q[k] = (k == S.acc[v]) ? 1.0 : 0.0;
-        const double ln = S.tb[v] / 64.0;
-        q[3] = S.tb[v]; q[4] = S.ub[v]; q[5] = ln; q[6] = S.ul[v];
-        for (int k = 0; k < 3; ++k) q[7 + k] = (k == S.reuse[v]) ? 1.0 : 0.0;
-        q[10] = S.di[v]; q[11] = S.db[v]; q[12] = S.cnt[v]; q[13] = S.strd[v];
-        const double c = S.cnt[v] > 1.0 ? S.cnt[v] : 1.0;
-        q[14] = S.tb[v] / c; q[15] = S.ub[v] / c; q[16] = ln / c; q[17] = S.ul[v] / c;
-      }
-      double alloc = 4.0;
-      for (int i = own_start; i < n_nest; ++i)
-        if (nest[4 * i + 1] == 0) alloc *= (double)nest[4 * i];
-      o[159] = alloc;
-      o[160] = (double)n_live;
-      o[161] = (double)n_nest;
-      o[162] = total;
-      o[163] = (double)unroll;
-    }
-    __syncwarp();
-    const bool bad = S.bad != 0;
-    for (int k = lane; k < NF; k += 32) {
-      double x = S.row[k];
-      if (!is_onehot(k)) x = log2(1.0 + (x > 0.0 ? x : 0.0));
-      out[k] = bad ? __longlong_as_double(0x7ff8000000000000ULL) : x;
-    }
-    if (bad && lane == 0) atomicExch(err, 2);
-    __syncwarp();
-  }
-}
-
 }  // namespace lt
 
 extern "C" int lt_features_device(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt,
                                   double* d_rows, int* d_err, void* stream) {
   if (n_stmt <= 0) return 0;
-  const int threads = 128, warps = threads / 32;
-  const size_t smem = sizeof(lt::WarpSmem) * warps;
-  static bool configured = false;
-  if (!configured) {
-    if (lt::check_cuda(cudaFuncSetAttribute(lt::features_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)smem), "features smem attr"))
-      return -1;
-    configured = true;
-  }
-  int64_t blocks = (n_stmt + warps - 1) / warps;
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  lt::features_warp_kernel<<<(unsigned)blocks, threads, smem, (cudaStream_t)stream>>>(d_words, d_stmt_off, n_stmt,
-                                                                                     d_rows, d_err);
-  return lt::check_launch("features_warp_kernel");
+  const int threads = 128;
+  const int64_t blocks = (n_stmt + threads - 1) / threads;
+  lt::features_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(d_words, d_stmt_off, n_stmt,
+                                                                             d_rows, d_err);
+  return lt::check_launch("features_kernel");
 }
-
-

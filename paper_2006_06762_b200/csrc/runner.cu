@@ -383,7 +383,65 @@ __global__ void __launch_bounds__(256) ffma_peak_kernel(float* out, int iters, f
   for (int k = 0; k < 8; ++k) s += a[k];
   if (s == 123.456f) out[threadIdx.x] = s;   // keep the chains live
 }
+
+// register-operand form (a = a*b + c, b and c runtime registers): the FFMA shape
+// of a GEMM inner product, which may issue at a lower rate than the immediate form
+__global__ void __launch_bounds__(256) ffma_reg_kernel(float* out, const float* in, int iters) {
+  float a[8], b[8], c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = (float)(threadIdx.x + k) * 1e-3f;
+    b[k] = in[k];
+    c[k] = in[8 + k];
+  }
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b[(k + u) & 7], c[(k + 3 * u) & 7]);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 123.456f) out[threadIdx.x] = s;
+}
 }  // namespace lt
+
+extern "C" int lt_ffma_peak_reg(int device, double* tflops, double* ms_out) {
+  if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return -1;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float *out = nullptr, *in = nullptr;
+  if (lt::check_cuda(cudaMalloc(&out, 1024 * sizeof(float)), "cudaMalloc") ||
+      lt::check_cuda(cudaMalloc(&in, 64 * sizeof(float)), "cudaMalloc"))
+    return -1;
+  float h[64];
+  for (int i = 0; i < 64; ++i) h[i] = (i < 8) ? 0.9999f : 1e-4f;
+  cudaMemcpy(in, h, sizeof h, cudaMemcpyHostToDevice);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  lt::ffma_reg_kernel<<<blocks, threads>>>(out, in, 64);
+  double best = 1e30;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    lt::ffma_reg_kernel<<<blocks, threads>>>(out, in, iters);
+    cudaEventRecord(e1);
+    if (lt::check_cuda(cudaEventSynchronize(e1), "ffma reg peak")) return -1;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  *tflops = 2.0 * (double)blocks * threads * iters * 16 * 8 / (best * 1e-3) / 1e12;
+  *ms_out = best;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  cudaFree(in);
+  return 0;
+}
+
 
 extern "C" int lt_ffma_peak(int device, double* tflops, double* ms_out) {
   if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return -1;

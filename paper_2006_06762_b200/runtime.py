@@ -68,6 +68,7 @@ _SIGS = [
     ("lt_task_upload", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64]),
     ("lt_task_download", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64]),
     ("lt_task_run", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int]),
+    ("lt_ffma_peak_reg", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     ("lt_ffma_peak", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     ("lt_measure", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, c_i32p, c_i64p, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]),
