@@ -281,7 +281,7 @@ def main() -> None:
         return ms
 
     run_steps(0, args.warmup, False)                               # warm-up (NVRTC workers, clocks)
-    runner.stats.update({"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0})
+    runner.stats.update({k: 0 if isinstance(v, int) else 0.0 for k, v in runner.stats.items()})
     with Clocks(local) as clk:
         ms = run_steps(args.warmup, args.steps, False)
     stats = dict(runner.stats)
@@ -291,7 +291,7 @@ def main() -> None:
     # our kernels launched in the timed region: per measured candidate, its kernels x
     # (warm-up + repeats), plus one NaN-poison and one verification launch per output
     n_launch = sum(len(r.info.get("kernels", [])) * (1 + r.repeats) + 2 * r.n_outputs
-                   for r in timed_records if r.repeats)
+                   for r in timed_records if r.n_outputs)
     io1 = dict(runner.io)
     e2e_ms = run_steps(args.warmup + args.steps, args.steps, True)
     io2 = dict(runner.io)
@@ -335,6 +335,7 @@ def main() -> None:
             "best_program": {"us": best_us, "tflops": achieved, "flop": FLOPS[args.config]},
             "compile": {"compiled": stats["compiled"], "cache_hits": stats["cache_hits"],
                         "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
+            "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s")},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "kernel": "best candidate of the timed steps (cost = mean of CUDA-event repeats)",

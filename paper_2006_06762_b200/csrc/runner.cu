@@ -347,11 +347,18 @@ int lt_measure(int64_t handle, const lt_launch* launches, int n_launch, const in
   float err;
   memcpy(&err, &bits, 4);
   rec->max_rel_err = err;
-  // 4. timed repeats
+  // 4. timed repeats: a run at least min_ms long is its own measurement (min_repeat
+  //    0); shorter kernels are re-run until the timed region spans min_ms
   double first_ms = ms > 1e-4 ? ms : 1e-4;
   int r = (int)ceil(min_ms / first_ms);
+  if (first_ms >= min_ms) r = 0;
   if (r < min_repeat) r = min_repeat;
   if (r > max_repeat) r = max_repeat;
+  if (r == 0) {
+    rec->repeats = 0;
+    rec->cost_us = first_ms * 1000.0;
+    return 0;
+  }
   cudaEventRecord(t->ev0, t->stream);
   for (int k = 0; k < r; ++k)
     if (launch_list(t, launches, n_launch, why)) return lt::fail(why);

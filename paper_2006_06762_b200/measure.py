@@ -8,6 +8,10 @@ Per candidate: `validate` (host, reference messages) -> lower to CUDA
 ground truth on the device (max relative error <= `GPU_TOL`, the north star's
 1e-4 for fp32) -> time with CUDA events.  `cost` is device microseconds.
 
+Timing: one warm-up run (also verified), then, if it was shorter than
+`min_ms` (1 ms), timed repeats until the timed region spans `min_ms`; a run of
+at least `min_ms` is its own measurement.  CUDA events on the task stream.
+
 Statuses: INVALID (validation failure, no legal launch, compile/launch
 failure, or wrong output — detail says which), TIMEOUT (cost >=
 `limits.cost_ceiling`, read in microseconds), VALID.  Throughput is
@@ -201,7 +205,7 @@ class Runner:
 
     def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
                  min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0,
-                 min_repeat: int = 1, backend: str = "ptx"):
+                 min_repeat: int = 0, backend: str = "ptx"):
         self.lib = rt.load()
         self.device = device
         rt.check(self.lib.lt_set_device(device), "set device")
@@ -218,7 +222,8 @@ class Runner:
         self.mod_lock = threading.Lock()
         self.failed_keys: dict = {}
         self._drain_error = None
-        self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0}
+        self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0,
+                      "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0}
         self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
 
@@ -301,6 +306,7 @@ class Runner:
     def measure_programs(self, programs: list, seed: int = 0) -> list:
         """Validate + lower on this thread while a measurement thread drains
         finished compiles onto the GPU (ctypes drops the GIL inside lt_measure)."""
+        t_start = time.perf_counter()
         recs = [Record() for _ in programs]
         for p in programs:                       # device contexts are created up front
             self.context(p.dag, seed)
@@ -322,6 +328,7 @@ class Runner:
                     recs[i].lower_s = time.perf_counter() - t0
                     continue
                 recs[i].lower_s = time.perf_counter() - t0
+                self.stats["lower_s"] += recs[i].lower_s
                 recs[i].info = lo.info
                 key = hashlib.sha1(lo.source.encode()).hexdigest()
                 with self.mod_lock:
@@ -341,6 +348,7 @@ class Runner:
             err, self._drain_error = self._drain_error, None
             raise err
         self.last_records = recs
+        self.stats["wall_s"] += time.perf_counter() - t_start
         return recs
 
     def _ready(self, item) -> bool:
@@ -369,7 +377,9 @@ class Runner:
                 if idx is None:
                     if closed and not waiting:
                         return
-                    time.sleep(0.001)
+                    t0 = time.perf_counter()
+                    time.sleep(0.0005)
+                    self.stats["idle_s"] += time.perf_counter() - t0
                     continue
                 self._measure_one(waiting.pop(idx), recs, seed)
         except BaseException as e:          # surfaced on the calling thread
@@ -399,9 +409,13 @@ class Runner:
                 with self.mod_lock:
                     self.failed_keys[key] = rec.detail
                 return
+            t0 = time.perf_counter()
             funcs = self.load(key, data, entries)
+            self.stats["load_s"] += time.perf_counter() - t0
         ctx = self.context(p.dag, seed)
+        t0 = time.perf_counter()
         m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        self.stats["gpu_s"] += time.perf_counter() - t0
         self.stats["measured"] += 1
         self.io["d2h"] += 4                                 # the max-relative-error word
         rec.first_us, rec.repeats = m.first_us, m.repeats
