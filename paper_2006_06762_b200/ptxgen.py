@@ -20,17 +20,22 @@ identical verdicts and outputs.
 from __future__ import annotations
 
 import math
+import os
 import struct
+
+import numpy as np
 
 from .lower import (
     MAX_ACC, MAX_SMEM, MAX_THREADS, MAX_UNROLLED, MAX_VTHREAD, NAIVE_THREADS, Buffer, Kernel,
-    Lowered, LoweringError, _attached, _binding, _must_materialize, _reads_buffer, _unroll_flags,
+    Lowered, LoweringError, _attached, _binding, _must_materialize, _reads_buffer, _unroll_flags, promote_register_tile,
     _written, ident, tile_levels,
 )
 from .state.expr import kind, reads
 
 
 LOOKAHEAD = 64      # statements between a shared-memory load and its first use
+# template switches (all on in production; LT_PTX_OFF=promote,plan,pad turns them off for A/B checks)
+_OFF = set(os.environ.get("LT_PTX_OFF", "").split(","))
 
 
 class Unsupported(Exception):
@@ -388,6 +393,39 @@ class _Kern:
         g(f"{pred}ld.global.nc.{g.ft} {f}, [{rb}+{imm}];")
         return g.remember(key, f)
 
+    def gbase(self, name: str) -> str:
+        """Pointer register of an unpacked global buffer (registers it as a parameter)."""
+        m = self.m
+        if name not in m.live and name not in m.buffers:
+            m.buffers[name] = Buffer(name, m.shape(name), "input")
+        return self.param(name)
+
+    def gload_at(self, ptr: str, off: Aff, const: int, guard) -> str:
+        """Load element `ptr + off + const` (off: runtime element offset)."""
+        g = self.g
+        key = ("gld@", ptr, off.key(), const, guard)
+        hit = g.cached(key)
+        if hit:
+            return hit
+        if off.terms:
+            k2 = ("gptr@", ptr, off.key())
+            rb = g.cached(k2)
+            if rb is None:
+                o = g.aff(off.runtime())
+                w = g.new("%rd")
+                g(f"mul.wide.s32 {w}, {o}, {g.esz};")
+                rb = g.new("%rd")
+                g(f"add.s64 {rb}, {ptr}, {w};")
+                g.remember(k2, rb)
+        else:
+            rb = ptr
+        f = g.new(g.fr)
+        pred = f"@{guard} " if guard else ""
+        if guard:
+            g(f"mov.b{32 if g.ft == 'f32' else 64} {f}, 0;")
+        g(f"{pred}ld.global.nc.{g.ft} {f}, [{rb}+{const * g.esz}];")
+        return g.remember(key, f)
+
     def gstore(self, name: str, idx: list, val: str) -> None:
         g = self.g
         base = self.param(name)
@@ -589,27 +627,34 @@ def _args(k: _Kern, mod: _Mod, s) -> list:
     return list(k.params)
 
 
-def _smem_strides(hull: list, lane_coords, order=None, step: int = 1) -> tuple:
+def _bank_degree(coord_sets, st) -> int:
+    banks: dict = {}
+    for coords in coord_sets:
+        addr = sum(c * s_ for c, s_ in zip(coords, st))
+        banks.setdefault(addr % 32, set()).add(addr)
+    return max(len(v) for v in banks.values()) if banks else 1
+
+
+def _smem_strides(hull: list, lane_coords, order=None, step: int = 1, store_coords=None) -> tuple:
     """Strides (indexed by hull dim) of a staged tile laid out in `order`
     (outer->inner), innermost dim padded by a multiple of `step` to minimise
-    shared-memory bank conflicts of the warp's first access."""
+    shared-memory bank conflicts of the warp's first compute-side access, then
+    of the cooperative fetch's stores (`store_coords`: the tile coordinates the
+    warp's lanes store in one fetch instruction)."""
     order = list(range(len(hull))) if order is None else order
     best = None
-    for pad in range(0, 9, step):
+    for pad in range(0, 33, step):
         st = [0] * len(hull)
         m = 1
         for j, d in enumerate(reversed(order)):
             st[d] = m
             m *= hull[d] + (pad if j == 0 else 0)
-        banks: dict = {}
-        for coords in lane_coords:
-            addr = sum(c * s_ for c, s_ in zip(coords, st))
-            banks.setdefault(addr % 32, set()).add(addr)
-        deg = max(len(v) for v in banks.values()) if banks else 1
-        cand = (deg, m, pad)
+        deg = _bank_degree(lane_coords, st)
+        sdeg = _bank_degree(store_coords, st) if store_coords else 1
+        cand = (deg, sdeg, m, pad)
         if best is None or cand < best[0]:
             best = (cand, st, m)
-        if deg == 1:
+        if deg == 1 and sdeg == 1:
             break
     return best[1], best[2]
 
@@ -737,6 +782,9 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             unrolled *= x[2]
     if unrolled > MAX_UNROLLED:
         raise LoweringError(f"unrolled body of {unrolled} statements exceeds {MAX_UNROLLED}")
+    if "promote" not in _OFF:
+        unroll = promote_register_tile([x[2] for x in loop_list], unroll, [x[1][0] == "S" for x in loop_list],
+                                       n_acc, n_threads)
     # the accumulator tile is indexed only by space-level digits: it stays in
     # registers whenever those loops are unrolled (rolled reduction loops are fine)
     acc_in_regs = all(u for x, u in zip(loop_list, unroll) if x[1][0] == "S")
@@ -784,7 +832,16 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                         v += cc * loc
                 c.append(v)
             coords.append(c)
-        o["stride"], o["words"] = _smem_strides(o["hull"], coords, o["order"], o["vec"])
+        scoords = []
+        for ln in range(lanes):
+            c, x = [], ln
+            for h in reversed(o["hull"]):
+                c.append(x % h)
+                x //= h
+            if x == 0:
+                scoords.append(c[::-1])
+        o["stride"], o["words"] = _smem_strides(o["hull"], coords, o["order"], o["vec"],
+                                                None if "pad" in _OFF else scoords)
         total_words = -(-total_words // 4) * 4          # 16-byte aligned operand bases
         o["base_word"] = total_words
         total_words += o["words"]
@@ -841,23 +898,93 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
 
     stage_axes = [(r, f(r, stage_lv[0])) for r in red if f(r, stage_lv[0]) > 1]
 
+    def operand_base(o, sdig):
+        base = []
+        for lin in o["read"].index:
+            b = Aff.k(lin.const)
+            for n, c in lin.terms:
+                if n in T:
+                    mn = digit(n, ("S", 0)).scale(T[n])
+                else:
+                    mn = sdig(n).scale(RT[n])
+                b = b + (mn.scale(c) if c >= 0 else (mn + (span[n] - 1)).scale(c))
+            base.append(b)
+        return base
+
+    def carry_free_shifts(o, trips):
+        """Per fetch trip t, the constant hull-coordinate shift with
+        coords(tid + t*threads) == coords(tid) + shift for every live tid, or
+        None when some tid carries across a hull digit."""
+        hull = o["hull"]
+        tids = np.arange(n_threads, dtype=np.int64)
+
+        def digits(e):
+            out, x = [], e.copy()
+            for h in reversed(hull):
+                out.append(x % h)
+                x //= h
+            out.append(x)             # overflow beyond the outermost dim
+            return np.stack(out[::-1], axis=1)
+        d0 = digits(tids)
+        shifts = []
+        for t in range(trips):
+            e = tids + t * n_threads
+            live = e < o["size"]
+            if not live.any():
+                return None
+            dd = digits(e)[live] - d0[live]
+            if (dd != dd[0]).any() or dd[0][0] != 0:
+                return None
+            shifts.append([int(x) for x in dd[0][1:]])
+        return shifts
+
+    # loop-invariant part of the cooperative fetch (coordinates, tail predicates,
+    # shared-memory addresses, global pointers without the staging offset),
+    # emitted once before the staging loop
+    fetch_plan: dict = {}
+
+    def prep_fetch():
+        zero = lambda r: Aff.k(0)  # noqa: E731
+        for oi, o in enumerate(operands):
+            trips = -(-o["size"] // n_threads)
+            if trips > 16 or "plan" in _OFF:
+                continue
+            full = o["size"] % n_threads == 0
+            shifts = carry_free_shifts(o, trips)
+            cs0 = g.decompose(tid, o["hull"]) if shifts is not None else None
+            base0 = operand_base(o, zero)
+            name = o["read"].buffer
+            plain = name not in attached_prod and (name in mod.live or mod.layouts.get(name) is None)
+            for t in range(trips):
+                tail = None
+                if not full and t == trips - 1:
+                    tail = g.new("%p")
+                    g(f"setp.lt.s32 {tail}, {tid}, {o['size'] - t * n_threads};")
+                if shifts is not None:
+                    cs = [Aff.reg(c) + sh for c, sh in zip(cs0, shifts[t])]
+                else:
+                    cs = [Aff.reg(c) for c in g.decompose(g.aff(Aff.reg(tid) + t * n_threads), o["hull"])]
+                saddr = Aff.k(o["base_word"])
+                for c, st_ in zip(cs, o["stride"]):
+                    saddr = saddr + c.scale(st_)
+                srt = saddr.runtime()
+                sreg = g.aff(srt) if srt.terms else None
+                ptr = None
+                if plain:
+                    gb = k.gbase(name)
+                    flat = k.gflat(name, [b_ + c for b_, c in zip(base0, cs)])
+                    ptr, imm = g.gaddr(gb, flat)
+                    ptr = (ptr, flat.const)
+                fetch_plan[(oi, t)] = (cs, tail, (sreg, saddr.const), ptr)
+
     def fetch_load(sdig, pnext=None):
         """Issue the global loads (and inline producer math) of one staging step;
-        returns (value, shared word address register, predicate) per element."""
+        returns (value, shared word address (register, const), predicate) per element."""
         items = []
-        for o in operands:
+        for oi, o in enumerate(operands):
             r = o["read"]
             hull = o["hull"]
-            base = []
-            for di, lin in enumerate(r.index):
-                b = Aff.k(lin.const)
-                for n, c in lin.terms:
-                    if n in T:
-                        mn = digit(n, ("S", 0)).scale(T[n])
-                    else:
-                        mn = sdig(n).scale(RT[n])
-                    b = b + (mn.scale(c) if c >= 0 else (mn + (span[n] - 1)).scale(c))
-                base.append(b)
+            base = operand_base(o, sdig)
             trips = -(-o["size"] // n_threads)
             full = o["size"] % n_threads == 0
 
@@ -878,10 +1005,33 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 saddr = Aff.k(o["base_word"])
                 for c, st_ in zip(cs, o["stride"]):
                     saddr = saddr + Aff.reg(c, st_)
-                items.append((v, g.aff(saddr), pt))
+                items.append((v, (g.aff(saddr), 0), pt))
+
+            def planned(t, o=o, oi=oi, r=r, base=base):
+                cs, tail, sa, ptr = fetch_plan[(oi, t)]
+                pt = pnext
+                if tail is not None:
+                    pt = tail
+                    if pnext is not None:
+                        pt = g.new("%p")
+                        g(f"and.pred {pt}, {tail}, {pnext};")
+                idx = [b_ + c for b_, c in zip(base, cs)]
+                if ptr is None:
+                    v = (k.producer(r.buffer, idx, pt) if r.buffer in attached_prod
+                         else k.gload(r.buffer, idx, pt))
+                else:
+                    # global address = hoisted pointer + staging offset (shared by all trips)
+                    flat = k.gflat(r.buffer, idx)
+                    inv = k.gflat(r.buffer, [b_ + c for b_, c in zip(operand_base(o, lambda n: Aff.k(0)), cs)])
+                    stage_part = flat + inv.scale(-1)
+                    v = k.gload_at(ptr[0], stage_part, flat.const, pt)
+                items.append((v, sa, pt))
             if trips <= 16:
                 for t in range(trips):
-                    elem(Aff.reg(tid) + t * n_threads, not full and t == trips - 1)
+                    if (oi, t) in fetch_plan:
+                        planned(t)
+                    else:
+                        elem(Aff.reg(tid) + t * n_threads, not full and t == trips - 1)
             else:
                 def run(tv, o=o, full=full, elem=elem):
                     elem(Aff.reg(tid) + tv.scale(n_threads), not full)
@@ -890,11 +1040,18 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         return items
 
     def fetch_store(items, buf):
-        for v, sa, pt in items:
-            a = g.new("%r")
-            g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {buf};")
+        for v, (sa, sc), pt in items:
+            key = ("sst", sa, buf)
+            a = g.cached(key)
+            if a is None:
+                a = g.new("%r")
+                if sa is None:
+                    g(f"mov.u32 {a}, {buf};")
+                else:
+                    g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {buf};")
+                g.remember(key, a)
             pred = f"@{pt} " if pt else ""
-            g(f"{pred}st.shared.{g.ft} [{a}], {v};")
+            g(f"{pred}st.shared.{g.ft} [{a}+{sc * g.esz}], {v};")
 
     # address coefficients: shared-memory word address of operand o as
     #   const0 + sum over local level digits (axis, level) of coef * digit
@@ -1103,6 +1260,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     trips_all = [-(-o["size"] // n_threads) for o in operands]
     double = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
+    prep_fetch()
     if not double:
         def stage_rec(i, sd):
             if i == len(stage_axes):
@@ -1182,7 +1340,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     info = {"template": "tiled", "stage": s.name, "structure": structure, "threads": n_threads,
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
             "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx",
-            "double_buffered": double}
+            "double_buffered": double, "acc_in_regs": acc_in_regs, "n_stage": n_stage}
     return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
 
 
