@@ -80,6 +80,14 @@ class Aff:
         return tuple(sorted(self.terms.items()))
 
 
+def _reg_order(item):
+    reg = item[0]
+    i = len(reg)
+    while i and reg[i - 1].isdigit():
+        i -= 1
+    return (reg[:i], int(reg[i:]) if i < len(reg) else -1)
+
+
 def _magic(d):
     L = (d - 1).bit_length()
     return -(-(1 << (31 + L)) // d), L - 1
@@ -146,7 +154,9 @@ class Ptx:
         if hit:
             return hit
         r = None
-        for reg, c in sorted(a.terms.items()):
+        # oldest registers first: the loop-invariant prefix of the chain is then
+        # hoistable by ptxas out of rolled loops
+        for reg, c in sorted(a.terms.items(), key=_reg_order if "order" not in _OFF else None):
             if r is None:
                 if c == 1:
                     r = reg
@@ -337,6 +347,8 @@ class _Kern:
         self.ptr: dict = {}             # buffer -> 64-bit global pointer register
         self.writes: set = set()
         self.body: list = []
+        self.vec_stores = False         # set for fully unrolled epilogues
+        self.pending: list = []
 
     def param(self, name: str) -> str:
         if name not in self.ptr:
@@ -430,8 +442,36 @@ class _Kern:
         g = self.g
         base = self.param(name)
         self.writes.add(name)
-        rb, imm = g.gaddr(base, self.gflat(name, idx))
-        g(f"st.global.{g.ft} [{rb}+{imm}], {val};")
+        flat = self.gflat(name, idx)
+        rb, imm = g.gaddr(base, flat)
+        if not self.vec_stores or g.ft != "f32":
+            g(f"st.global.{g.ft} [{rb}+{imm}], {val};")
+            return
+        # 16-byte alignment of rb holds when every runtime coefficient is a
+        # multiple of 4 elements (buffers are cudaMalloc'd, 256-byte aligned)
+        aligned = all(c % 4 == 0 for c in flat.runtime().terms.values())
+        self.pending.append((rb, imm, val, aligned))
+        self.drain_stores(False)
+
+    def drain_stores(self, final: bool) -> None:
+        """Emit pending epilogue stores, four consecutive aligned words as one
+        st.global.v4 (the register tile's innermost run along the output's
+        contiguous dim)."""
+        g, P = self.g, self.pending
+        while P:
+            rb, imm, val, al = P[0]
+            run = al and imm % 16 == 0
+            k = 1
+            while run and k < len(P) and k < 4 and P[k][0] == rb and P[k][1] == imm + 4 * k:
+                k += 1
+            if run and k == 4:
+                g(f"st.global.v4.f32 [{rb}+{imm}], {{{', '.join(x[2] for x in P[:4])}}};")
+                del P[:4]
+                continue
+            if run and not final and k == len(P):
+                return                  # the run may still complete
+            g(f"st.global.f32 [{rb}+{imm}], {val};")
+            del P[0]
 
     # -- inline producers and readers ---------------------------------------
     def reader(self, stage, iv, override=None):
@@ -1329,13 +1369,19 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 rb, imm = _local_addr(g, ab, ai)
                 val = g.new(g.fr)
                 g(f"ld.local.{g.ft} {val}, [{rb}+{imm}];")
-            g.push()
-            k.epilogue(s, idx_of, val, _must_materialize(mod, s))
-            g.pop()
+            if acc_in_regs:     # straight-line: addresses are shared across the tile
+                k.epilogue(s, idx_of, val, _must_materialize(mod, s))
+            else:
+                g.push()
+                k.epilogue(s, idx_of, val, _must_materialize(mod, s))
+                g.pop()
             return
         a, lv, ext = reg_loops[i]
         k.loop(ext, acc_in_regs, lambda r: ep(i + 1, {**dg, (a, lv): r}))
+    k.vec_stores = acc_in_regs and "vst" not in _OFF
     ep(0, {})
+    k.drain_stores(True)
+    k.vec_stores = False
 
     info = {"template": "tiled", "stage": s.name, "structure": structure, "threads": n_threads,
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
