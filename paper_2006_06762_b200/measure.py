@@ -31,6 +31,8 @@ import threading
 import json
 import math
 import os
+import pickle
+import sys
 import time
 from collections import OrderedDict
 from dataclasses import dataclass, field, replace
@@ -204,12 +206,37 @@ class _DagContext:
         return out
 
 
+def _lower_one(p, backend: str):
+    """validate + lower one State (runs in a lowering worker process).
+    Returns (kind, payload, seconds): ("bad", detail) | ("err", detail) | ("ok", Lowered)."""
+    t0 = time.perf_counter()
+    bad = validate(p)
+    if bad:
+        return "bad", bad[0], 0.0
+    try:
+        lo = None
+        if backend == "ptx":
+            try:
+                lo = lower_ptx(p)
+            except Unsupported:
+                pass
+        if lo is None:
+            lo = lower(p)
+    except LoweringError as e:
+        return "err", f"gpu: {e}", time.perf_counter() - t0
+    return "ok", lo, time.perf_counter() - t0
+
+
 class Runner:
-    """Per-process GPU runner: one device, one compile pool, DAG contexts, module cache."""
+    """Per-process GPU runner: one device, one compile pool, DAG contexts, module cache.
+
+    Host work per candidate (validate + lowering, pure Python) runs in a pool of
+    lowering processes so it neither serialises the batch nor holds the GIL the
+    measurement thread needs between device calls."""
 
     def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
                  min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0,
-                 min_repeat: int = 0, backend: str = "ptx"):
+                 min_repeat: int = 0, backend: str = "ptx", lower_workers: int | None = None):
         self.lib = rt.load()
         self.device = device
         rt.check(self.lib.lt_set_device(device), "set device")
@@ -230,8 +257,25 @@ class Runner:
                       "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0}
         self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
+        self.lower_workers = (lower_workers if lower_workers is not None
+                              else int(os.environ.get("LT_LOWER_WORKERS", max(1, min(8, (os.cpu_count() or 2) // 2)))))
+        self._lpool = None
+
+    def _lower_pool(self):
+        main = sys.modules.get("__main__")
+        main_file = getattr(main, "__file__", None)
+        if main_file is not None and not os.path.exists(main_file):
+            return None             # spawn cannot re-import a stdin/REPL __main__: lower in-process
+        if self._lpool is None and self.lower_workers > 1:
+            import multiprocessing as mp
+            from concurrent.futures import ProcessPoolExecutor
+            self._lpool = ProcessPoolExecutor(self.lower_workers, mp_context=mp.get_context("spawn"))
+        return self._lpool
 
     def close(self):
+        if self._lpool is not None:
+            self._lpool.shutdown(wait=False, cancel_futures=True)
+            self._lpool = None
         for m, _ in self.modules.values():
             self.lib.lt_module_unload(m)
         self.modules.clear()
@@ -320,20 +364,13 @@ class Runner:
         worker.start()
         batch_keys: dict = {}
         try:
-            for i, p in enumerate(programs):
-                bad = validate(p)
-                if bad:
-                    recs[i].detail = bad[0]
+            for i, p, (kind_, payload, secs) in self._lowered(programs):
+                recs[i].lower_s = secs
+                self.stats["lower_s"] += secs
+                if kind_ != "ok":
+                    recs[i].detail = payload
                     continue
-                t0 = time.perf_counter()
-                try:
-                    lo = self.lower(p)
-                except LoweringError as e:
-                    recs[i].detail = f"gpu: {e}"
-                    recs[i].lower_s = time.perf_counter() - t0
-                    continue
-                recs[i].lower_s = time.perf_counter() - t0
-                self.stats["lower_s"] += recs[i].lower_s
+                lo = payload
                 recs[i].info = lo.info
                 key = hashlib.sha1(lo.source.encode()).hexdigest()
                 with self.mod_lock:
@@ -355,6 +392,28 @@ class Runner:
         self.last_records = recs
         self.stats["wall_s"] += time.perf_counter() - t_start
         return recs
+
+    def _lowered(self, programs: list):
+        """(index, program, lowering result) in completion order."""
+        pool = self._lower_pool() if len(programs) > 1 else None
+        done: set = set()
+        if pool is not None:
+            from concurrent.futures import as_completed
+            from concurrent.futures.process import BrokenProcessPool
+            try:
+                futs = {pool.submit(_lower_one, p, self.backend): i for i, p in enumerate(programs)}
+                for f in as_completed(futs):
+                    i = futs[f]
+                    res = f.result()
+                    done.add(i)
+                    yield i, programs[i], res
+                return
+            except (BrokenProcessPool, OSError, pickle.PicklingError) as e:    # host-side only: lower here
+                self._lpool = None
+                self.stats["lower_pool_error"] = repr(e)
+        for i, p in enumerate(programs):
+            if i not in done:
+                yield i, p, _lower_one(p, self.backend)
 
     def _ready(self, item) -> bool:
         job = item[4]

@@ -19,6 +19,7 @@ identical verdicts and outputs.
 
 from __future__ import annotations
 
+import itertools
 import math
 import os
 import struct
@@ -330,6 +331,28 @@ class _Mod:
         self.live = {s.name: s for s in p.stages if not s.inlined}
         self.layouts = dict(p.layouts)
         self.buffers: dict = {}
+        self._att: dict = {}
+        self._rd: dict = {}
+        self._mm: dict = {}
+
+    def attached(self, host: str) -> list:
+        hit = self._att.get(host)
+        if hit is None:
+            hit = self._att[host] = _attached(self.p, host)
+        return hit
+
+    def reads(self, expr, name: str) -> bool:
+        key = (id(expr), name)
+        hit = self._rd.get(key)
+        if hit is None:
+            hit = self._rd[key] = _reads_buffer(expr, name)
+        return hit
+
+    def must_materialize(self, stage) -> bool:
+        hit = self._mm.get(stage.name)
+        if hit is None:
+            hit = self._mm[stage.name] = _must_materialize(self, stage)
+        return hit
 
     def shape(self, name):
         if name in self.live:
@@ -475,7 +498,7 @@ class _Kern:
 
     # -- inline producers and readers ---------------------------------------
     def reader(self, stage, iv, override=None):
-        attached_prod = {s.name for s in _attached(self.m.p, stage.name) if _reads_buffer(stage.expr, s.name)}
+        attached_prod = {s.name for s in self.m.attached(stage.name) if self.m.reads(stage.expr, s.name)}
 
         def read(buf, idx, guard):
             if override is not None:
@@ -547,8 +570,8 @@ class _Kern:
         space = [n for n, _ in host.space]
         if materialize:
             self.gstore(host.name, [idx_of[n] for n in space], value)
-        for c in _attached(self.m.p, host.name):
-            if not _reads_buffer(c.expr, host.name) or _reads_buffer(host.expr, c.name):
+        for c in self.m.attached(host.name):
+            if not self.m.reads(c.expr, host.name) or self.m.reads(host.expr, c.name):
                 continue
             cspace = [n for n, _ in c.space]
             if len(cspace) != len(space) or c.reduce:
@@ -653,7 +676,7 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
     else:
         expr = s.expr.body if kind(s.expr) == "Reduce" else s.expr
         value = Expr(g, lambda n: env[n], k.reader(s, lambda n: env[n]))(expr)
-    k.epilogue(s, {n: env[n] for n in space_names}, value, _must_materialize(mod, s))
+    k.epilogue(s, {n: env[n] for n in space_names}, value, mod.must_materialize(s))
     g.pop()
     g(f"add.s32 {pidx}, {pidx}, {grid * NAIVE_THREADS};")
     g(f"setp.lt.s32 {pe}, {pidx}, {total};")
@@ -782,7 +805,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         key = (r.buffer, tuple((l.terms, l.const) for l in r.index))
         if key not in [o["key"] for o in operands]:
             operands.append({"key": key, "read": r})
-    attached_prod = {c.name for c in _attached(mod.p, s.name) if _reads_buffer(s.expr, c.name)}
+    attached_prod = {c.name for c in mod.attached(s.name) if mod.reads(s.expr, c.name)}
     span = {**T, **RT}
     for o in operands:
         hull, off = [], []
@@ -1357,6 +1380,24 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # epilogue over the register tile
     reg_loops = [(a, lv, f(a, lv)) for lv in reg_levels for a in space if f(a, lv) > 1]
 
+    mustm = mod.must_materialize(s)
+    if acc_in_regs:
+        # straight-line epilogue: every register-level digit is a constant, so each
+        # element's index is a shared runtime base plus a compile-time offset
+        reg_set = set(reg_levels)
+        base_idx = {a: mixed(a, "S", 0, lambda a_, lv: Aff.k(0) if lv in reg_set else digit(a_, lv))
+                    for a in space}
+        k.vec_stores = "vst" not in _OFF
+        for combo in itertools.product(*[range(ext) for _, _, ext in reg_loops]):
+            off = dict.fromkeys(space, 0)
+            ai = 0
+            for (a, lv, _), val in zip(reg_loops, combo):
+                off[a] += val * mult(a, lv)
+                ai += acc_coef.get((a, lv), 0) * val
+            k.epilogue(s, {a: base_idx[a] + off[a] for a in space}, acc[ai], mustm)
+        k.drain_stores(True)
+        k.vec_stores = False
+
     def ep(i, dg):
         if i == len(reg_loops):
             def dgf(a, lv):
@@ -1369,19 +1410,14 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 rb, imm = _local_addr(g, ab, ai)
                 val = g.new(g.fr)
                 g(f"ld.local.{g.ft} {val}, [{rb}+{imm}];")
-            if acc_in_regs:     # straight-line: addresses are shared across the tile
-                k.epilogue(s, idx_of, val, _must_materialize(mod, s))
-            else:
-                g.push()
-                k.epilogue(s, idx_of, val, _must_materialize(mod, s))
-                g.pop()
+            g.push()
+            k.epilogue(s, idx_of, val, mustm)
+            g.pop()
             return
         a, lv, ext = reg_loops[i]
-        k.loop(ext, acc_in_regs, lambda r: ep(i + 1, {**dg, (a, lv): r}))
-    k.vec_stores = acc_in_regs and "vst" not in _OFF
-    ep(0, {})
-    k.drain_stores(True)
-    k.vec_stores = False
+        k.loop(ext, False, lambda r: ep(i + 1, {**dg, (a, lv): r}))
+    if not acc_in_regs:
+        ep(0, {})
 
     info = {"template": "tiled", "stage": s.name, "structure": structure, "threads": n_threads,
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,

@@ -27,6 +27,8 @@ def main() -> None:
     ap.add_argument("--backend", default="ptx")
     ap.add_argument("--configs", default="RC,G10,CL,TBG")
     ap.add_argument("--out", default="")
+    ap.add_argument("--offset", type=int, default=0)
+    ap.add_argument("--no-hand", action="store_true")
     args = ap.parse_args()
     from bench import FLOPS, load_stream
     from hand_states import states
@@ -36,7 +38,7 @@ def main() -> None:
     lines = []
     for cfg in args.configs.split(","):
         dag, stream = load_stream(cfg)
-        progs = [replay(dag, h) for h in stream[:args.k]]
+        progs = [replay(dag, h) for h in stream[args.offset:args.offset + args.k]]
         recs = r.measure_programs(progs)
         tf = [FLOPS[cfg] / (x.cost_us * 1e-6) / 1e12 for x in recs if x.status == "valid"]
         bad = [x.status + ":" + x.detail[:60] for x in recs if x.status != "valid"]
@@ -52,7 +54,7 @@ def main() -> None:
             lines.append({"cand": cfg, "i": i, "status": x.status, "us": x.cost_us,
                           "kernels": [{k: v for k, v in kk.items() if k != "factors"} | {"factors": kk.get("factors")}
                                       for kk in x.info.get("kernels", [])]})
-    for name, p in states():
+    for name, p in ([] if args.no_hand else states()):
         (rec,) = r.measure_programs([p])
         cfg = name.split()[0]
         line = {"hand": name, "status": rec.status, "us": rec.cost_us,
