@@ -155,11 +155,11 @@ def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
     sp = stream.cuda_stream
 
     def feats():
-        rt.check(lib.lt_features_device(d_words.data_ptr(), d_soff.data_ptr(), n_stmt, d_rows.data_ptr(),
+        rt.check(lib.lt_features_device_cm(d_words.data_ptr(), d_soff.data_ptr(), n_stmt, d_rows.data_ptr(),
                                         d_err.data_ptr(), sp), "features")
 
     def trees():
-        rt.check(lib.lt_predict_rows_device(h, d_rows.data_ptr(), n_stmt, d_rs.data_ptr(), sp), "trees")
+        rt.check(lib.lt_predict_cols_device(h, d_rows.data_ptr(), n_stmt, d_rs.data_ptr(), sp), "trees")
         rt.check(lib.lt_segment_sum_device(d_rs.data_ptr(), d_poff.data_ptr(), n_prog, d_sc.data_ptr(), sp), "sum")
 
     out = {}

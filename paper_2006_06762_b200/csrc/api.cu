@@ -11,7 +11,10 @@
 #include "common.h"
 
 extern "C" int lt_features_device(const int32_t*, const int64_t*, int64_t, double*, int*, void*);
+extern "C" int lt_features_device_cm(const int32_t*, const int64_t*, int64_t, double*, int*, void*);
+extern "C" int lt_cols_to_rows_device(const double*, int64_t, double*, void*);
 extern "C" int lt_predict_rows_device(int64_t, const double*, int64_t, double*, void*);
+extern "C" int lt_predict_cols_device(int64_t, const double*, int64_t, double*, void*);
 extern "C" int lt_segment_sum_device(const double*, const int64_t*, int64_t, double*, void*);
 
 namespace lt {
@@ -21,14 +24,14 @@ void set_error(const std::string& msg) { g_err = msg; }
 int fail(const std::string& msg) { g_err = msg; return -1; }
 
 struct Scratch {
-  DevBuf words, stmt_off, rows, row_scores, prog_off, scores, err;
+  DevBuf words, stmt_off, rows, cols, row_scores, prog_off, scores, err;
   cudaStream_t stream = nullptr;
   int init() {
     if (!stream && check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream")) return -1;
     return 0;
   }
   void release() {
-    for (DevBuf* b : {&words, &stmt_off, &rows, &row_scores, &prog_off, &scores, &err}) {
+    for (DevBuf* b : {&words, &stmt_off, &rows, &cols, &row_scores, &prog_off, &scores, &err}) {
       if (b->ptr) cudaFree(b->ptr);
       b->ptr = nullptr;
       b->cap = 0;
@@ -40,17 +43,24 @@ struct Scratch {
 static Scratch g_s;
 static std::mutex g_mu;
 
+// features of the uploaded records into g_s.cols ([164][n_stmt], column-major)
 static int upload_features(const int32_t* words, const int64_t* stmt_off, int64_t n_stmt) {
   int64_t n_words = stmt_off[n_stmt];
   if (g_s.init() || g_s.words.reserve((size_t)n_words * 4 + 4) ||
-      g_s.stmt_off.reserve((size_t)(n_stmt + 1) * 8) || g_s.rows.reserve((size_t)n_stmt * 164 * 8 + 8) ||
+      g_s.stmt_off.reserve((size_t)(n_stmt + 1) * 8) || g_s.cols.reserve((size_t)n_stmt * 164 * 8 + 8) ||
       g_s.err.reserve(4))
     return -1;
   cudaMemcpyAsync(g_s.words.ptr, words, (size_t)n_words * 4, cudaMemcpyHostToDevice, g_s.stream);
   cudaMemcpyAsync(g_s.stmt_off.ptr, stmt_off, (size_t)(n_stmt + 1) * 8, cudaMemcpyHostToDevice, g_s.stream);
   cudaMemsetAsync(g_s.err.ptr, 0, 4, g_s.stream);
-  return lt_features_device(g_s.words.as<int32_t>(), g_s.stmt_off.as<int64_t>(), n_stmt, g_s.rows.as<double>(),
-                            g_s.err.as<int>(), g_s.stream);
+  return lt_features_device_cm(g_s.words.as<int32_t>(), g_s.stmt_off.as<int64_t>(), n_stmt, g_s.cols.as<double>(),
+                               g_s.err.as<int>(), g_s.stream);
+}
+
+// g_s.cols -> g_s.rows ([n_stmt][164]) for callers that want rows on the host
+static int rows_from_cols(int64_t n_stmt) {
+  if (g_s.rows.reserve((size_t)n_stmt * 164 * 8 + 8)) return -1;
+  return lt_cols_to_rows_device(g_s.cols.as<double>(), n_stmt, g_s.rows.as<double>(), g_s.stream);
 }
 
 static int check_feature_err() {
@@ -82,7 +92,7 @@ int lt_set_device(int device) { return lt::check_cuda(cudaSetDevice(device), "cu
 int lt_features_batch(const int32_t* words, const int64_t* stmt_off, int64_t n_stmt, double* out_rows) {
   std::lock_guard<std::mutex> g(lt::g_mu);
   if (n_stmt <= 0) return 0;
-  if (lt::upload_features(words, stmt_off, n_stmt)) return -1;
+  if (lt::upload_features(words, stmt_off, n_stmt) || lt::rows_from_cols(n_stmt)) return -1;
   if (lt::check_feature_err()) return -1;
   cudaMemcpyAsync(out_rows, lt::g_s.rows.ptr, (size_t)n_stmt * 164 * 8, cudaMemcpyDeviceToHost, lt::g_s.stream);
   return lt::check_cuda(cudaStreamSynchronize(lt::g_s.stream), "features copy-back");
@@ -121,15 +131,17 @@ int lt_score_batch(int64_t model, const int32_t* words, const int64_t* stmt_off,
       s.scores.reserve((size_t)n_prog * 8))
     return -1;
   cudaMemcpyAsync(s.prog_off.ptr, prog_row_off, (size_t)(n_prog + 1) * 8, cudaMemcpyHostToDevice, s.stream);
-  if (n_stmt > 0 && lt_predict_rows_device(model, s.rows.as<double>(), n_stmt, s.row_scores.as<double>(), s.stream))
+  if (n_stmt > 0 && lt_predict_cols_device(model, s.cols.as<double>(), n_stmt, s.row_scores.as<double>(), s.stream))
     return -1;
   if (lt_segment_sum_device(s.row_scores.as<double>(), s.prog_off.as<int64_t>(), n_prog, s.scores.as<double>(),
                             s.stream))
     return -1;
   if (n_stmt > 0 && lt::check_feature_err()) return -1;
   cudaMemcpyAsync(out_scores, s.scores.ptr, (size_t)n_prog * 8, cudaMemcpyDeviceToHost, s.stream);
-  if (out_rows && n_stmt > 0)
+  if (out_rows && n_stmt > 0) {
+    if (lt::rows_from_cols(n_stmt)) return -1;
     cudaMemcpyAsync(out_rows, s.rows.ptr, (size_t)n_stmt * 164 * 8, cudaMemcpyDeviceToHost, s.stream);
+  }
   return lt::check_cuda(cudaStreamSynchronize(s.stream), "score copy-back");
 }
 

@@ -172,18 +172,22 @@ __device__ void annotation_block(const int32_t* nest, int n_nest, int ann, doubl
 
 __global__ void __launch_bounds__(128)
 features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off,
-                int64_t n_stmt, double* __restrict__ rows, int* __restrict__ err) {
+                int64_t n_stmt, double* __restrict__ rows, int64_t ld_col, int* __restrict__ err) {
+  // element (statement s, column k) lives at rows[s * ld_row + k * ld_col]:
+  // row-major (ld_col 1) or column-major (ld_col n_stmt, coalesced across the warp)
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n_stmt) return;
   const int32_t* r = words + stmt_off[s];
-  double* out = rows + s * NF;
+  const int64_t ld_row = ld_col == 1 ? NF : 1;
+  double* out = rows + s * ld_row;
+#define O(k) out[(int64_t)(k) * ld_col]
 
   const int n_nest = r[0], own_start = r[1], n_loops = r[2], n_iter = r[3], n_views = r[4];
   const int unroll = r[5], n_live = r[6], has_reduce = r[7];
   const int32_t* ops = r + 8;
   const int n_nodes = r[17];
   if (n_nest > MAX_NEST || n_loops > MAX_LOOPS || n_iter > MAX_ITERS || n_views > MAX_VIEWS) {
-    for (int i = 0; i < NF; ++i) out[i] = __longlong_as_double(0x7ff8000000000000ULL);
+    for (int i = 0; i < NF; ++i) O(i) = __longlong_as_double(0x7ff8000000000000ULL);
     atomicExch(err, 1);
     return;
   }
@@ -324,11 +328,14 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
   }
 
   // ---- row assembly (src/features.py:388-417) ----
+  // every column is written once, already compressed: log2(1 + max(x, 0)) on the
+  // non-one-hot columns (src/features.py:416)
+  auto W = [&](int k, double x) { O(k) = is_onehot(k) ? x : log2(1.0 + (x > 0.0 ? x : 0.0)); };
   double b[11];
-  for (int k = 0; k < 9; ++k) out[k] = (double)ops[k] * total;
-  for (int k = 9; k < 18; ++k) out[k] = 0.0;
+  for (int k = 0; k < 9; ++k) W(k, (double)ops[k] * total);
+  for (int k = 9; k < 18; ++k) O(k) = 0.0;
   annotation_block(nest, n_nest, 2, b);
-  for (int k = 0; k < 11; ++k) out[18 + k] = b[k];
+  for (int k = 0; k < 11; ++k) W(18 + k, b[k]);
   {  // unroll block
     for (int k = 0; k < 11; ++k) b[k] = 0.0;
     long long prod = 1;
@@ -345,13 +352,13 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
     }
     if (!n_cov) b[1] = 1.0;
     else { b[0] = (double)nest[4 * first]; b[1 + tag] = 1.0; b[9] = (double)prod; b[10] = (double)n_cov; }
-    for (int k = 0; k < 11; ++k) out[29 + k] = b[k];
+    for (int k = 0; k < 11; ++k) W(29 + k, b[k]);
   }
   annotation_block(nest, n_nest, 1, b);
-  for (int k = 0; k < 11; ++k) out[40 + k] = b[k];
-  for (int k = 51; k < 59; ++k) out[k] = 0.0;
+  for (int k = 0; k < 11; ++k) W(40 + k, b[k]);
+  for (int k = 51; k < 59; ++k) O(k) = 0.0;
   if (n_nest == 0 || ops_total == 0) {
-    for (int k = 59; k < 69; ++k) out[k] = 0.0;
+    for (int k = 59; k < 69; ++k) O(k) = 0.0;
   } else {
     double inside[MAX_NEST + 1];
     inside[n_nest] = 1.0;
@@ -364,7 +371,7 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
       if (pos == 0) { by = 0.0; for (int v = 0; v < n_views; ++v) by += ub[v]; }
       else by = ws[pos - 1];
       double flops = (double)ops_total * inside[pos];
-      out[58 + j] = flops / (by > 1.0 ? by : 1.0);
+      W(58 + j, flops / (by > 1.0 ? by : 1.0));
     }
   }
   // ranked buffer blocks: by (-total_bytes, name)
@@ -372,8 +379,8 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
   for (int v = 0; v < n_views; ++v) used[v] = false;
   int n_rank = n_views < 5 ? n_views : 5;
   for (int slot = 0; slot < 5; ++slot) {
-    double* o = out + 69 + 18 * slot;
-    if (slot >= n_rank) { for (int k = 0; k < 18; ++k) o[k] = 0.0; continue; }
+    const int o = 69 + 18 * slot;
+    if (slot >= n_rank) { for (int k = 0; k < 18; ++k) O(o + k) = 0.0; continue; }
     int best = -1;
     for (int v = 0; v < n_views; ++v) {
       if (used[v]) continue;
@@ -381,40 +388,74 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
     }
     used[best] = true;
     const int v = best;
-    for (int k = 0; k < 3; ++k) o[k] = (k == acc[v]) ? 1.0 : 0.0;
+    for (int k = 0; k < 3; ++k) O(o + k) = (k == acc[v]) ? 1.0 : 0.0;
     double ln = tb[v] / 64.0;
-    o[3] = tb[v]; o[4] = ub[v]; o[5] = ln; o[6] = ul[v];
-    for (int k = 0; k < 3; ++k) o[7 + k] = (k == reuse[v]) ? 1.0 : 0.0;
-    o[10] = di[v]; o[11] = db[v]; o[12] = cnt[v]; o[13] = strd[v];
+    W(o + 3, tb[v]); W(o + 4, ub[v]); W(o + 5, ln); W(o + 6, ul[v]);
+    for (int k = 0; k < 3; ++k) O(o + 7 + k) = (k == reuse[v]) ? 1.0 : 0.0;
+    W(o + 10, di[v]); W(o + 11, db[v]); W(o + 12, cnt[v]); W(o + 13, strd[v]);
     double c = cnt[v] > 1.0 ? cnt[v] : 1.0;
-    o[14] = tb[v] / c; o[15] = ub[v] / c; o[16] = ln / c; o[17] = ul[v] / c;
+    W(o + 14, tb[v] / c); W(o + 15, ub[v] / c); W(o + 16, ln / c); W(o + 17, ul[v] / c);
   }
-  out[159] = alloc;
-  out[160] = (double)n_live;
-  out[161] = (double)n_nest;
-  out[162] = total;
-  out[163] = (double)unroll;
-
-  // log2(1 + max(x, 0)) on every non-one-hot column
-  for (int k = 0; k < NF; ++k) {
-    if (is_onehot(k)) continue;
-    double x = out[k];
-    out[k] = log2(1.0 + (x > 0.0 ? x : 0.0));
-  }
+  W(159, alloc);
+  W(160, (double)n_live);
+  W(161, (double)n_nest);
+  W(162, total);
+  W(163, (double)unroll);
   if (!ok) {
-    for (int i = 0; i < NF; ++i) out[i] = __longlong_as_double(0x7ff8000000000000ULL);
+    for (int i = 0; i < NF; ++i) O(i) = __longlong_as_double(0x7ff8000000000000ULL);
     atomicExch(err, 2);
   }
+#undef O
 }
 
 }  // namespace lt
 
-extern "C" int lt_features_device(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt,
-                                  double* d_rows, int* d_err, void* stream) {
+static int launch_features(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt, double* d_out,
+                           int64_t ld_col, int* d_err, void* stream) {
   if (n_stmt <= 0) return 0;
   const int threads = 128;
   const int64_t blocks = (n_stmt + threads - 1) / threads;
   lt::features_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(d_words, d_stmt_off, n_stmt,
-                                                                             d_rows, d_err);
+                                                                             d_out, ld_col, d_err);
   return lt::check_launch("features_kernel");
+}
+
+// rows[n_stmt][164] (row-major)
+extern "C" int lt_features_device(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt,
+                                  double* d_rows, int* d_err, void* stream) {
+  return launch_features(d_words, d_stmt_off, n_stmt, d_rows, 1, d_err, stream);
+}
+
+// cols[164][n_stmt] (column-major: each warp's stores are contiguous)
+extern "C" int lt_features_device_cm(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt,
+                                     double* d_cols, int* d_err, void* stream) {
+  return launch_features(d_words, d_stmt_off, n_stmt, d_cols, n_stmt, d_err, stream);
+}
+
+namespace lt {
+// [164][n] -> [n][164] through a shared-memory tile (coalesced on both sides)
+__global__ void __launch_bounds__(256) cols_to_rows_kernel(const double* __restrict__ cols, int64_t n,
+                                                          double* __restrict__ rows) {
+  __shared__ double tile[32][33];
+  const int64_t s0 = (int64_t)blockIdx.x * 32;
+  const int k0 = blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += 8) {
+    int k = k0 + dy;
+    int64_t s = s0 + threadIdx.x;
+    if (k < NF && s < n) tile[dy][threadIdx.x] = cols[(int64_t)k * n + s];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += 8) {
+    int64_t s = s0 + dy;
+    int k = k0 + threadIdx.x;
+    if (k < NF && s < n) rows[s * NF + k] = tile[threadIdx.x][dy];
+  }
+}
+}  // namespace lt
+
+extern "C" int lt_cols_to_rows_device(const double* d_cols, int64_t n, double* d_rows, void* stream) {
+  if (n <= 0) return 0;
+  dim3 grid((unsigned)((n + 31) / 32), (lt::NF + 31) / 32), block(32, 8);
+  lt::cols_to_rows_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(d_cols, n, d_rows);
+  return lt::check_launch("cols_to_rows_kernel");
 }

@@ -40,16 +40,23 @@ struct Model {
 };
 
 __global__ void __launch_bounds__(ROWS_PER_BLOCK)
-predict_rows_kernel(const double* __restrict__ X, int64_t n_rows, const Node* __restrict__ nodes,
+predict_rows_kernel(const double* __restrict__ X, int64_t n_rows, bool col_major, const Node* __restrict__ nodes,
                     const int32_t* __restrict__ tree_off, int n_trees, const int32_t* __restrict__ used,
                     int n_used, double base, double* __restrict__ out) {
   extern __shared__ double tile[];             // ROWS_PER_BLOCK x (n_used + 1)
   const int ld = n_used + 1;                   // odd stride: conflict-free row access
   const int64_t row0 = (int64_t)blockIdx.x * ROWS_PER_BLOCK;
   const int rows_here = (int)min((int64_t)ROWS_PER_BLOCK, n_rows - row0);
-  for (int e = threadIdx.x; e < rows_here * n_used; e += blockDim.x) {
-    int r = e / n_used, c = e - r * n_used;
-    tile[r * ld + c] = X[(row0 + r) * NF + used[c]];
+  if (col_major) {            // X[164][n_rows]: consecutive threads read consecutive rows
+    for (int e = threadIdx.x; e < rows_here * n_used; e += blockDim.x) {
+      int c = e / rows_here, r = e - c * rows_here;
+      tile[r * ld + c] = X[(int64_t)used[c] * n_rows + row0 + r];
+    }
+  } else {
+    for (int e = threadIdx.x; e < rows_here * n_used; e += blockDim.x) {
+      int r = e / n_used, c = e - r * n_used;
+      tile[r * ld + c] = X[(row0 + r) * NF + used[c]];
+    }
   }
   __syncthreads();
   const int r = threadIdx.x;
@@ -181,8 +188,8 @@ int lt_model_info(int64_t handle, int* n_trees, int* n_used_features) {
   return 0;
 }
 
-int lt_predict_rows_device(int64_t handle, const double* d_rows, int64_t n_rows, double* d_row_scores,
-                           void* stream) {
+static int predict_device(int64_t handle, const double* d_rows, int64_t n_rows, bool col_major,
+                          double* d_row_scores, void* stream) {
   Model* m = (Model*)(intptr_t)handle;
   if (!m) return lt::fail("null model");
   if (n_rows <= 0) return 0;
@@ -196,8 +203,21 @@ int lt_predict_rows_device(int64_t handle, const double* d_rows, int64_t n_rows,
   }
   int64_t blocks = (n_rows + lt::ROWS_PER_BLOCK - 1) / lt::ROWS_PER_BLOCK;
   lt::predict_rows_kernel<<<(unsigned)blocks, lt::ROWS_PER_BLOCK, smem, (cudaStream_t)stream>>>(
-      d_rows, n_rows, m->d_nodes, m->d_tree_off, m->n_trees, m->d_used, m->n_used, m->base, d_row_scores);
+      d_rows, n_rows, col_major, m->d_nodes, m->d_tree_off, m->n_trees, m->d_used, m->n_used, m->base,
+      d_row_scores);
   return lt::check_launch("predict_rows_kernel");
+}
+
+// rows[n_rows][164]
+int lt_predict_rows_device(int64_t handle, const double* d_rows, int64_t n_rows, double* d_row_scores,
+                           void* stream) {
+  return predict_device(handle, d_rows, n_rows, false, d_row_scores, stream);
+}
+
+// cols[164][n_rows] (the layout lt_features_device_cm writes)
+int lt_predict_cols_device(int64_t handle, const double* d_cols, int64_t n_rows, double* d_row_scores,
+                           void* stream) {
+  return predict_device(handle, d_cols, n_rows, true, d_row_scores, stream);
 }
 
 int lt_segment_sum_device(const double* d_row_scores, const int64_t* d_prog_off, int64_t n_prog,

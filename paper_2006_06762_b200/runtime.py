@@ -34,12 +34,17 @@ _SIGS = [
     ("lt_features_batch", ctypes.c_int, [c_i32p, c_i64p, ctypes.c_int64, c_f64p]),
     ("lt_features_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p]),
+    ("lt_features_device_cm", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                             ctypes.c_void_p, ctypes.c_void_p]),
+    ("lt_cols_to_rows_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]),
     ("lt_model_create", ctypes.c_int64, [ctypes.c_int, c_i64p, c_i32p, c_f64p, c_i32p, c_i32p, c_f64p, c_f64p,
                                          ctypes.c_double, ctypes.c_int]),
     ("lt_model_destroy", None, [ctypes.c_int64]),
     ("lt_model_info", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("lt_predict_batch", ctypes.c_int, [ctypes.c_int64, c_f64p, c_i64p, ctypes.c_int64, c_f64p]),
     ("lt_predict_rows_device", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
+                                              ctypes.c_void_p]),
+    ("lt_predict_cols_device", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                               ctypes.c_void_p]),
     ("lt_segment_sum_device", ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                              ctypes.c_void_p]),

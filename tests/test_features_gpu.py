@@ -64,3 +64,36 @@ def test_pairwise_sum_order_many_rows():
     for g, X in zip(got, mats):
         rows = np.where(X[:, 0] <= 0.5, 1e16, 1.0)
         assert g == float(rows.sum())
+
+
+def test_column_major_features_and_predict_match_row_major(corpus):
+    """lt_features_device_cm (+ lt_cols_to_rows_device) and lt_predict_cols_device
+    are bit-identical to the row-major entry points on the golden corpus."""
+    import torch
+    from paper_2006_06762_b200 import runtime as rt
+    from paper_2006_06762_b200.encode import encode_batch
+    from paper_2006_06762_b200.model import GpuCostModel
+    lib = rt.load()
+    words, soff, _ = encode_batch(corpus.programs)
+    n = len(soff) - 1
+    dev = torch.device("cuda", 0)
+    d_w, d_so = torch.from_numpy(words).to(dev), torch.from_numpy(soff).to(dev)
+    rows = torch.empty((n, 164), dtype=torch.float64, device=dev)
+    cols = torch.empty((164, n), dtype=torch.float64, device=dev)
+    back = torch.empty((n, 164), dtype=torch.float64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    sp = torch.cuda.current_stream().cuda_stream
+    rt.check(lib.lt_features_device(d_w.data_ptr(), d_so.data_ptr(), n, rows.data_ptr(), err.data_ptr(), sp), "rm")
+    rt.check(lib.lt_features_device_cm(d_w.data_ptr(), d_so.data_ptr(), n, cols.data_ptr(), err.data_ptr(), sp), "cm")
+    rt.check(lib.lt_cols_to_rows_device(cols.data_ptr(), n, back.data_ptr(), sp), "transpose")
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert torch.equal(rows, back)
+    assert torch.equal(rows.t().contiguous(), cols)
+    m = GpuCostModel.from_json(corpus.model_json)
+    a = torch.empty(n, dtype=torch.float64, device=dev)
+    b = torch.empty(n, dtype=torch.float64, device=dev)
+    rt.check(lib.lt_predict_rows_device(m.handle(), rows.data_ptr(), n, a.data_ptr(), sp), "rows")
+    rt.check(lib.lt_predict_cols_device(m.handle(), cols.data_ptr(), n, b.data_ptr(), sp), "cols")
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

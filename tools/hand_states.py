@@ -53,6 +53,12 @@ def states():
     out.append(("RC 4x8x28 co64", tiled(rc, "C", {"cn": (1, 1, 1, 1), "ch": (1, 4, 1, 1), "cw": (2, 7, 1, 2),
                                                   "cc": (2, 8, 1, 4)},
                                         {"rh": (1, 1), "rw": (1, 3), "rc": (1, 8)})))
+    tbg = config_dag("TBG")
+    # batched GEMM: 1 batch x 64x64 per block, 16x16 threads, 4x4 per thread, k tile 16
+    out.append(("TBG 64x64/256thr/4x4", tiled(tbg, "C", {"b": (1, 1, 1, 1), "i": (1, 16, 1, 4), "j": (1, 16, 1, 4)},
+                                              {"k": (1, 16)})))
+    out.append(("TBG 128x64/256thr/8x4", tiled(tbg, "C", {"b": (1, 1, 1, 1), "i": (2, 16, 1, 4),
+                                                          "j": (1, 16, 1, 4)}, {"k": (1, 8)})))
     return out
 
 
