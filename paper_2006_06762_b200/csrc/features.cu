@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <math.h>
+#include <stdlib.h>
 #include "common.h"
 
 namespace lt {
@@ -43,14 +44,20 @@ __device__ __forceinline__ long long fmod_(long long a, long long c) {
   return r;
 }
 
+// upper bound of own loop j (lo = 0): its full range when pos < 0, else its range
+// only if the loop sits inside nest position pos (`ws_inside`, src/features.py:266-274)
+__device__ __forceinline__ long long loop_hi(const int32_t* loops, int j, int pos) {
+  return (pos < 0 || loops[3 * j + 2] > pos) ? (long long)loops[3 * j] - 1 : 0;
+}
+
 // interval of one postfix decode AST given per-own-loop upper bounds (lo = 0)
-__device__ bool ast_interval(const int32_t* nodes, int cnt, const long long* hi, Iv& out) {
+__device__ bool ast_interval(const int32_t* nodes, int cnt, const int32_t* loops, int pos, Iv& out) {
   Iv st[MAX_STACK];
   int sp = 0;
   for (int n = 0; n < cnt; ++n) {
     int op = nodes[2 * n], arg = nodes[2 * n + 1];
     switch (op) {
-      case 0: if (sp >= MAX_STACK) return false; st[sp].lo = 0; st[sp].hi = hi[arg]; ++sp; break;
+      case 0: if (sp >= MAX_STACK) return false; st[sp].lo = 0; st[sp].hi = loop_hi(loops, arg, pos); ++sp; break;
       case 1: if (sp >= MAX_STACK) return false; st[sp].lo = arg; st[sp].hi = arg; ++sp; break;
       case 2: { if (sp < 2) return false; Iv b = st[--sp]; st[sp - 1].lo += b.lo; st[sp - 1].hi += b.hi; break; }
       case 3: { if (sp < 1) return false; Iv a = st[sp - 1]; long long c = arg;
@@ -68,13 +75,14 @@ __device__ bool ast_interval(const int32_t* nodes, int cnt, const long long* hi,
   return true;
 }
 
-__device__ bool ast_eval(const int32_t* nodes, int cnt, const long long* env, long long& out) {
+// value of a decode AST with every own loop at 0 except loop `one_at` at 1
+__device__ bool ast_eval(const int32_t* nodes, int cnt, int one_at, long long& out) {
   long long st[MAX_STACK];
   int sp = 0;
   for (int n = 0; n < cnt; ++n) {
     int op = nodes[2 * n], arg = nodes[2 * n + 1];
     switch (op) {
-      case 0: if (sp >= MAX_STACK) return false; st[sp++] = env[arg]; break;
+      case 0: if (sp >= MAX_STACK) return false; st[sp++] = (arg == one_at) ? 1 : 0; break;
       case 1: if (sp >= MAX_STACK) return false; st[sp++] = arg; break;
       case 2: if (sp < 2) return false; --sp; st[sp - 1] += st[sp]; break;
       case 3: if (sp < 1) return false; st[sp - 1] *= arg; break;
@@ -170,13 +178,12 @@ __device__ void annotation_block(const int32_t* nest, int n_nest, int ann, doubl
   b[10] = (double)hits;
 }
 
-__global__ void __launch_bounds__(128)
-features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off,
-                int64_t n_stmt, double* __restrict__ rows, int64_t ld_col, int* __restrict__ err) {
-  // element (statement s, column k) lives at rows[s * ld_row + k * ld_col]:
-  // row-major (ld_col 1) or column-major (ld_col n_stmt, coalesced across the warp)
-  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n_stmt) return;
+// One statement's 164-wide row.  Element (statement s, column k) lives at
+// rows[s * ld_row + k * ld_col]: row-major (ld_col 1) or column-major (ld_col
+// n_stmt, coalesced across the warp).
+__device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off,
+                                            int64_t s, double* __restrict__ rows, int64_t ld_col,
+                                            int* __restrict__ err) {
   const int32_t* r = words + stmt_off[s];
   const int64_t ld_row = ld_col == 1 ? NF : 1;
   double* out = rows + s * ld_row;
@@ -221,12 +228,10 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
   }
 
   // own-range intervals of every iterator decode
-  long long hi[MAX_LOOPS];
   Iv iv[MAX_ITERS];
-  for (int j = 0; j < n_loops; ++j) hi[j] = (long long)loops[3 * j] - 1;
   bool ok = true;
   for (int it = 0; it < n_iter; ++it)
-    ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], hi, iv[it]);
+    ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, -1, iv[it]);
 
   double total = 1.0;
   for (int i = 0; i < n_nest; ++i) total *= (double)nest[4 * i];
@@ -245,11 +250,9 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
   const int inner_own = (n_nest > own_start) ? nest[4 * (n_nest - 1) + 3] : -1;
   long long val0[MAX_ITERS], val1[MAX_ITERS];
   if (inner_own >= 0) {
-    long long env[MAX_LOOPS];
-    for (int j = 0; j < n_loops; ++j) env[j] = 0;
-    for (int it = 0; it < n_iter; ++it) ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], env, val0[it]);
-    env[inner_own] = 1;
-    for (int it = 0; it < n_iter; ++it) ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], env, val1[it]);
+    for (int it = 0; it < n_iter; ++it) ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], -1, val0[it]);
+    for (int it = 0; it < n_iter; ++it)
+      ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], inner_own, val1[it]);
   }
   for (int v = 0; v < n_views; ++v) {
     const View& w = views[v];
@@ -312,11 +315,9 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
   // working set inside each nest position (src/features.py:266-274)
   double ws[MAX_NEST];
   for (int pos = 0; pos < n_nest; ++pos) {
-    long long h2[MAX_LOOPS];
     Iv iv2[MAX_ITERS];
-    for (int j = 0; j < n_loops; ++j) h2[j] = loops[3 * j + 2] > pos ? (long long)loops[3 * j] - 1 : 0;
     for (int it = 0; it < n_iter; ++it)
-      ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], h2, iv2[it]);
+      ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, iv2[it]);
     double acc_ws = 0.0;
     for (int v = 0; v < n_views; ++v) {
       long long p = 1;
@@ -408,13 +409,34 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
 #undef O
 }
 
+// Persistent grid-stride loop: the grid is sized so that each thread's local
+// working set (intervals, per-view statistics, decode stacks) stays L1/L2
+// resident instead of spilling to HBM (SM count x blocks_per_sm blocks).
+__global__ void __launch_bounds__(128)
+features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off,
+                int64_t n_stmt, double* __restrict__ rows, int64_t ld_col, int* __restrict__ err) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n_stmt; s += stride)
+    feature_row(words, stmt_off, s, rows, ld_col, err);
+}
+
 }  // namespace lt
 
 static int launch_features(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt, double* d_out,
                            int64_t ld_col, int* d_err, void* stream) {
   if (n_stmt <= 0) return 0;
   const int threads = 128;
-  const int64_t blocks = (n_stmt + threads - 1) / threads;
+  static int sms = 0, per_sm = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* e = getenv("LT_FEAT_BLOCKS_PER_SM");
+    per_sm = e ? atoi(e) : 0;
+    cudaFuncSetAttribute(lt::features_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+  }
+  int64_t blocks = (n_stmt + threads - 1) / threads;
+  if (per_sm > 0 && blocks > (int64_t)sms * per_sm) blocks = (int64_t)sms * per_sm;
   lt::features_kernel<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(d_words, d_stmt_off, n_stmt,
                                                                              d_out, ld_col, d_err);
   return lt::check_launch("features_kernel");
