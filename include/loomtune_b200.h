@@ -70,6 +70,19 @@ int lt_segment_sum_device(const double* d_row_scores, const int64_t* d_prog_off,
 int lt_score_batch(int64_t model, const int32_t* words, const int64_t* stmt_off, int64_t n_stmt,
                    const int64_t* prog_row_off, int64_t n_prog, double* out_scores, double* out_rows);
 
+/* ---- (B) GBDT training ------------------------------------------------------
+ * Replaces `_fit_tree` (model.py:158-255), the inner loop of `train`
+ * (model.py:275-320).  lt_gbdt_create uploads a training matrix rows[n][nf]
+ * (host) and sorts every feature column once; lt_gbdt_fit_tree fits one tree
+ * for target[n], w[n] with the reference's exact split rule and numbering
+ * (arrays of capacity cap >= 2^(depth+1)-1; *n_nodes = node count).
+ * Bit-identical to the reference (numpy's summation orders).                 */
+int64_t lt_gbdt_create(const double* rows, int64_t n, int nf);
+void lt_gbdt_destroy(int64_t handle);
+int lt_gbdt_fit_tree(int64_t handle, const double* target, const double* w, int depth, int cap,
+                     int32_t* feature, double* threshold, int32_t* left, int32_t* right, double* value,
+                     int32_t* n_nodes);
+
 /* ---- (A) compile service ---------------------------------------------------
  * N NVRTC worker processes + on-disk cubin cache keyed by (options, source).
  * Candidate kernels are generated by paper_2006_06762_b200/lower.py. */

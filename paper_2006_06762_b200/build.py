@@ -25,6 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = {
     "features.cu": ["--fmad=false"],
     "predict.cu": ["--fmad=false"],
+    "gbdt.cu": ["--fmad=false"],
     "api.cu": [],
     "runner.cu": [],
     "compile_pool.cpp": [],

@@ -4,8 +4,10 @@
 (`src/sched.py:24-30`, `src/cli.py:25`):
 
 * `measure_batch`  -> `paper_2006_06762_b200.measure.measure_batch` (GPU runner);
-* `train`          -> the reference's own `train`, result wrapped as `GpuCostModel`
-                      (north star: the train interface stays unchanged);
+* `train`          -> `gbdt.train`: the same interface and a bit-identical model,
+                      with every tree fitted on the GPU (`csrc/gbdt.cu`);
+                      `install(..., gpu_train=False)` keeps the reference's own
+                      `train` and wraps its result as `GpuCostModel`;
 * `evolve`         -> `evolve_batched`: the reference's evolution loop
                       (`src/evolve.py:442-502`) verbatim in its random-number use,
                       except that each population is scored with one
@@ -117,8 +119,12 @@ def make_gpu_sampler(sample_program, tries: int = 64):
     return sample
 
 
-def install(loomtune, gpu_sampler: bool = False) -> dict:
-    """Rebind the reference's hot-path call sites; returns the originals."""
+def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True) -> dict:
+    """Rebind the reference's hot-path call sites; returns the originals.
+
+    gpu_train: `train` fits its trees on the GPU (`gbdt.train`, bit-identical
+    models); False keeps the reference's own `train` and
+    only wraps its result."""
     import importlib
     sched = importlib.import_module(loomtune.__name__ + ".sched")
     cli = importlib.import_module(loomtune.__name__ + ".cli")
@@ -128,6 +134,9 @@ def install(loomtune, gpu_sampler: bool = False) -> dict:
     ref_train = sched.train
 
     def train(records, hyper=None):
+        if gpu_train:
+            from . import gbdt
+            return gbdt.train(records, hyper)
         return GpuCostModel.wrap(ref_train(records, hyper) if hyper is not None else ref_train(records))
 
     sched.measure_batch = measure_batch

@@ -51,6 +51,11 @@ _SIGS = [
     ("lt_score_batch", ctypes.c_int, [ctypes.c_int64, c_i32p, c_i64p, ctypes.c_int64, c_i64p, ctypes.c_int64,
                                       c_f64p, c_f64p]),
     ("lt_release_scratch", None, []),
+    # GBDT training (csrc/gbdt.cu)
+    ("lt_gbdt_create", ctypes.c_int64, [c_f64p, ctypes.c_int64, ctypes.c_int]),
+    ("lt_gbdt_destroy", None, [ctypes.c_int64]),
+    ("lt_gbdt_fit_tree", ctypes.c_int, [ctypes.c_int64, c_f64p, c_f64p, ctypes.c_int, ctypes.c_int, c_i32p, c_f64p,
+                                        c_i32p, c_i32p, c_f64p, ctypes.POINTER(ctypes.c_int32)]),
     # compile pool (csrc/compile_pool.cpp)
     ("lt_pool_start", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_double]),
     ("lt_pool_stop", None, []),

@@ -81,3 +81,37 @@ def test_oracle_measure_batch_matches_reference(corpus):
             assert r.status == status and r.detail == detail
             assert (r.cost == math.inf) if cost == "inf" else (r.cost == cost)
             assert r.throughput == thr
+
+
+def _train_cases():
+    import json
+    import os
+    import numpy as np
+    from tests.golden_corpus import GOLDEN, load_corpus
+    c = load_corpus()
+    t = np.load(os.path.join(GOLDEN, "train.npz"))
+    mats = [c.features_of(i) for i in range(len(c.programs))]
+    out = [("corpus (tests/golden/model.json)", mats, t["y"], {"trees": 30, "depth": 6, "shrinkage": 0.3},
+            c.model_json, None)]
+    for case in json.load(open(os.path.join(GOLDEN, "train_models.json"))):
+        offs = case["offsets"]
+        if case["source"] == "corpus":
+            rows = c.rows
+        elif case["source"]:
+            rows = np.vstack([np.round(mats[i], 1) for i in range(0, len(mats), 3)])
+        else:
+            rows = np.asarray(case["rows"], np.float64)
+        m = [rows[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
+        out.append((case["name"], m, np.asarray(case["y"]), case["hyper"], case["model"], case["train_losses"]))
+    return out
+
+
+def test_oracle_train_reproduces_reference_models():
+    """oracle/train.py == the reference's own `train` on every golden case (exact)."""
+    from oracle import train as OT
+    for name, mats, y, hyper, want, losses in _train_cases():
+        got = OT.train(mats, y, **hyper)
+        got_losses = got.pop("train_losses")
+        assert got == want, name
+        if losses is not None:
+            assert got_losses == losses, name
