@@ -182,6 +182,50 @@ def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
     return out
 
 
+def traffic_of(sha1: str):
+    """DRAM bytes per launch of a profiled candidate (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            hit = json.load(fh).get(sha1)
+        return hit["dram_bytes_per_launch"] if hit else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def train_bench(n_prog: int = 1500) -> dict:
+    """GBDT training: `gbdt.train` (trees fitted on the
+    B200) vs the CPU restatement of the reference's `train` (oracle/train.py,
+    pinned to reference-trained golden models) on the same records: stream
+    States of the four configs, labels U(0.05, 1), default hyper (30 trees,
+    depth 6).  Models must be identical."""
+    import numpy as np
+    from oracle import train as OT
+    from paper_2006_06762_b200 import gbdt
+    from paper_2006_06762_b200.features import extract_features_batch
+    from paper_2006_06762_b200.model import Hyper
+    from paper_2006_06762_b200.state import replay
+
+    class Rec:
+        def __init__(self, f, y):
+            self.feats, self.y, self.dag_id = f, float(y), "d"
+    feats = []
+    for cfg in ("RC", "G10", "CL", "TBG"):
+        dag, stream = load_stream(cfg)
+        feats += extract_features_batch([replay(dag, h) for h in stream[:n_prog // 4]])
+    y = np.random.default_rng(0).uniform(0.05, 1.0, len(feats))
+    gbdt.train([Rec(f, v) for f, v in zip(feats[:50], y[:50])], Hyper(trees=2))       # warm-up
+    t0 = time.perf_counter()
+    got = gbdt.train([Rec(f, v) for f, v in zip(feats, y)], Hyper()).to_json()
+    gpu_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    want = OT.train(feats, y)
+    cpu_s = time.perf_counter() - t0
+    want.pop("train_losses")
+    return {"programs": len(feats), "rows": int(sum(len(f) for f in feats)), "trees": 30, "depth": 6,
+            "gpu_s": gpu_s, "cpu_s": cpu_s, "speedup": cpu_s / gpu_s, "identical": got == want,
+            "cpu_kind": "port (oracle/train.py, 1 core)"}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -303,6 +347,7 @@ def main() -> None:
     n_valid = sum(r.status == "valid" for rs in timed for r in rs)
     costs = [r.cost for rs in timed for r in rs if r.status == "valid"]
     best_us = min(costs) if costs else float("nan")
+    best_rec = min((r for r in timed_records if r.status == "valid"), key=lambda r: r.cost_us, default=None)
     value = n_total / (ms / 1000.0)
     e2e = (args.steps * B * world) / (e2e_ms / 1000.0)
     if world > 1:   # launches of all ranks
@@ -332,13 +377,19 @@ def main() -> None:
                        "compile_workers_per_rank": workers, "cubin_cache": "empty at start",
                        "l2": "inputs resident; no flush between repeats (Ansor measurement semantics)"},
             "valid": n_valid, "measured": n_total,
-            "best_program": {"us": best_us, "tflops": achieved, "flop": FLOPS[args.config]},
+            "best_program": {"us": best_us, "tflops": achieved, "flop": FLOPS[args.config],
+                             "source_sha1": best_rec.key if best_rec else None,
+                             "kernels": (best_rec.info.get("kernels") if best_rec else None)},
             "compile": {"compiled": stats["compiled"], "cache_hits": stats["cache_hits"],
                         "recompiled_O1": stats.get("recompiled", 0),
                         "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
             "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s")},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None,
+                         "traffic": traffic_of(best_rec.key if best_rec else ""),
+                         "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the best "
+                                         "candidate (ncu --set full, profiles/traffic.json by source sha1; "
+                                         "null when this run's best was not profiled)",
                          "kernel": "best candidate of the timed steps (cost = mean of CUDA-event repeats)",
                          "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU"},
             "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
@@ -349,6 +400,7 @@ def main() -> None:
         }
         line["clocks"] = clk.summary()
         if not args.no_scoring:
+            line["train"] = train_bench()
             progs = [replay(dag, h) for h in stream[:256]]
             sb = scoring_bench(local, progs)
             rows_bytes = sb["n_stmt"] * 164 * 8

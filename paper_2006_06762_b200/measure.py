@@ -86,6 +86,7 @@ class Record:
     lower_s: float = 0.0
     n_outputs: int = 0
     info: dict = field(default_factory=dict)
+    key: str = ""             # sha1 of the candidate's generated source
 
 
 def random_inputs(dag, seed: int) -> dict:
@@ -373,6 +374,7 @@ class Runner:
                 lo = payload
                 recs[i].info = lo.info
                 key = hashlib.sha1(lo.source.encode()).hexdigest()
+                recs[i].key = key
                 with self.mod_lock:
                     loaded = key in self.modules
                 if loaded:

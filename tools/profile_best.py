@@ -1,8 +1,11 @@
 """Profiling driver (run under ncu on the GPU box).
 
-  python tools/profile_best.py CFG N     measure the first N stream States of CFG,
+  python tools/profile_best.py CFG N [OFFSET]
+                                         measure N stream States of CFG from OFFSET
+                                         (bench.py's timed steps are RC 128 from 96),
                                          then re-launch the best one's kernels 3x
-                                         inside an NVTX range "profile"
+                                         inside an NVTX range "profile"; writes
+                                         gpurun_out/best_CFG.json (kernel hashes)
   python tools/profile_best.py --scoring  run the population-scoring kernels once
                                          inside the NVTX range
 
@@ -20,24 +23,27 @@ ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
 sys.path.insert(0, ROOT)
 
 
-def best_candidate(cfg: str, n: int) -> None:
+def best_candidate(cfg: str, n: int, offset: int = 0) -> None:
     import torch
     from bench import load_stream
     from paper_2006_06762_b200 import measure
     from paper_2006_06762_b200 import runtime as rt
-    from paper_2006_06762_b200.lower import lower
     from paper_2006_06762_b200.state import replay
     dag, stream = load_stream(cfg)
     runner = measure.configure(device=0, cache_dir="")
-    progs = [replay(dag, h) for h in stream[:n]]
+    progs = [replay(dag, h) for h in stream[offset:offset + n]]
     recs = runner.measure_programs(progs)
     best = min((r.cost_us, i) for i, r in enumerate(recs) if r.status == "valid")
     p = progs[best[1]]
-    lo = lower(p)
-    print(json.dumps({"config": cfg, "best_us": best[0], "index": best[1], "info": lo.info}), flush=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"best_{cfg}.cu"), "w") as fh:
-        fh.write(lo.source)
+    lo = runner.lower(p)
     key = __import__("hashlib").sha1(lo.source.encode()).hexdigest()
+    out = {"config": cfg, "best_us": best[0], "index": offset + best[1], "source_sha1": key,
+           "kernels": [k.entry for k in lo.kernels], "info": lo.info}
+    print(json.dumps(out), flush=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"best_{cfg}.json"), "w") as fh:
+        json.dump(out, fh)
+    with open(os.path.join(ROOT, "gpurun_out", f"best_{cfg}.src"), "w") as fh:
+        fh.write(lo.source)
     funcs = runner.load(key, b"", [k.entry for k in lo.kernels])
     ctx = runner.context(p.dag, 0)
     launches = ctx._launches(lo, funcs)
@@ -65,4 +71,4 @@ if __name__ == "__main__":
     if sys.argv[1] == "--scoring":
         scoring()
     else:
-        best_candidate(sys.argv[1], int(sys.argv[2]))
+        best_candidate(sys.argv[1], int(sys.argv[2]), int(sys.argv[3]) if len(sys.argv) > 3 else 0)
