@@ -310,8 +310,7 @@ def main() -> None:
         for ps in progs:
             if fresh_ctx:   # e2e: inputs re-uploaded and ground truth recomputed inside the region
                 for c in runner.ctx.values():
-                    runner.lib.lt_task_destroy(c.task)
-                runner.ctx.clear()
+                    c.refresh()
             res = sharded_measure(ps)          # NCCL all_gather of (status, cost) records
             all_recs.append(res)
             launch_log.append(list(runner.last_records))
@@ -394,8 +393,9 @@ def main() -> None:
                          "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU"},
             "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
                     "d2h_bytes_per_step": int(d2h_step),
-                    "note": "measure_batch on host Programs with a fresh DAG context per step: input tensors "
-                            "(fp32+fp64) and cubins H2D, fp64 ground truth recomputed, error words D2H"},
+                    "note": "measure_batch on host Programs; every step re-uploads the DAG's input tensors "
+                            "(fp32+fp64, pageable) and recomputes the fp64 ground truth on the device; cubins "
+                            "H2D; per-candidate error words D2H"},
             "gpu_launches": n_launch,
         }
         line["clocks"] = clk.summary()

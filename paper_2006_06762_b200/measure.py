@@ -140,9 +140,23 @@ class _DagContext:
         for name, b in ref.buffers.items():
             if b.role in ("temp", "output"):
                 self.slot(f"ref:{name}", b.numel * 8)
+        self._ref = (ref, funcs)
         launches = self._launches(ref, funcs, fp64=True)
         rt.check(lib.lt_task_run(self.task, ctypes.addressof(launches), len(ref.kernels)), "ground truth")
         self.outputs = list(ref.outputs)
+
+    def refresh(self) -> None:
+        """Re-upload every input (fp32 + fp64) into the existing slots, drop the
+        packed constants (re-packed and uploaded on next use) and recompute the
+        fp64 ground truth: the per-step host->device work of an end-to-end run."""
+        for name, arr in self.inputs.items():
+            self._upload(f"in:{name}", np.ascontiguousarray(arr, dtype=np.float32))
+            self._upload(f"in64:{name}", np.ascontiguousarray(arr, dtype=np.float64))
+        for key in [k for k in self.slots if k.startswith("pk:")]:
+            del self.slots[key]
+        ref, funcs = self._ref
+        launches = self._launches(ref, funcs, fp64=True)
+        rt.check(self.r.lib.lt_task_run(self.task, ctypes.addressof(launches), len(ref.kernels)), "ground truth")
 
     def slot(self, key: str, nbytes: int) -> int:
         if key not in self.slots:

@@ -371,6 +371,7 @@ class _Kern:
         self.writes: set = set()
         self.body: list = []
         self.vec_stores = False         # set for fully unrolled epilogues
+        self.store_guard = None         # predicate on epilogue stores (naive multi-point steps)
         self.pending: list = []
 
     def param(self, name: str) -> str:
@@ -468,7 +469,8 @@ class _Kern:
         flat = self.gflat(name, idx)
         rb, imm = g.gaddr(base, flat)
         if not self.vec_stores or g.ft != "f32":
-            g(f"st.global.{g.ft} [{rb}+{imm}], {val};")
+            pred = f"@{self.store_guard} " if self.store_guard else ""
+            g(f"{pred}st.global.{g.ft} [{rb}+{imm}], {val};")
             return
         # 16-byte alignment of rb holds when every runtime coefficient is a
         # multiple of 4 elements (buffers are cudaMalloc'd, 256-byte aligned)
@@ -586,6 +588,7 @@ class _Kern:
                     raise LoweringError(f"consumer {c.name} reads {host.name} at a non-identity index")
                 return None
             ex = Expr(g, lambda n: cenv[n], self.reader(c, lambda n: cenv[n], override=ov))
+            ex.guard = self.store_guard
             v = ex(c.expr)
             self.epilogue(c, {n: cenv[n] for n in cspace}, v, True)
 
@@ -604,7 +607,13 @@ class _Kern:
         return "\n".join(head + decl + self.body + loads + g.lines + ["  ret;", "}"]) + "\n"
 
 
+NAIVE_POINTS = 4        # output points per thread per grid-stride step (loads in flight)
+
+
 def _naive(mod: _Mod, s, entry: str) -> tuple:
+    """One output point per thread-iteration (the State's own loops and decode
+    maps, reductions serial), NAIVE_POINTS points per grid-stride step so each
+    thread keeps several independent loads / accumulation chains in flight."""
     k = _Kern(mod, entry, NAIVE_THREADS)
     g = k.g
     sp_loops = [l for l in s.loops if l.kind == "space"]
@@ -612,9 +621,11 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
     total = 1
     for l in sp_loops:
         total *= l.extent
-    if total >= (1 << 31):
+    U = NAIVE_POINTS if "naive4" not in _OFF else 1
+    if total + U * 148 * 16 * NAIVE_THREADS >= (1 << 31):
         raise Unsupported("index space exceeds 2^31")
-    grid = max(1, min((total + NAIVE_THREADS - 1) // NAIVE_THREADS, 148 * 16))
+    grid = max(1, min((total + NAIVE_THREADS * U - 1) // (NAIVE_THREADS * U), 148 * 16))
+    step = grid * NAIVE_THREADS
     dmap = dict(s.index_map)
     space_names = [n for n, _ in s.space]
     tid, cta, pidx = g.new("%r"), g.new("%r"), g.new("%r")
@@ -627,10 +638,6 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
     g(f"@{pe} bra {done};")
     g.label(top)
     g.push()
-    lv = {}
-    digits = g.decompose(pidx, [l.extent for l in sp_loops]) if sp_loops else []
-    for l, d in zip(sp_loops, digits):
-        lv[l.id] = Aff.reg(d)
 
     def dec(d, lv):
         kk = kind(d)
@@ -646,44 +653,72 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
         r = g.aff(a)
         return Aff.reg(g.udiv(r, d.c) if kk == "DDiv" else g.urem(r, d.c))
 
-    env = {n: dec(dmap[n], lv) for n in space_names if n in dmap}
+    # per point u: index, guard (u = 0 is in range inside the loop), decoded space env
+    pts = []
+    for u in range(U):
+        if u == 0:
+            pu, guard = pidx, None
+        else:
+            pu = g.new("%r")
+            g(f"add.s32 {pu}, {pidx}, {u * step};")
+            guard = g.new("%p")
+            g(f"setp.lt.s32 {guard}, {pu}, {total};")
+        lv = {}
+        digits = g.decompose(pu, [l.extent for l in sp_loops]) if sp_loops else []
+        for l, d in zip(sp_loops, digits):
+            lv[l.id] = Aff.reg(d)
+        pts.append((guard, lv, {n: dec(dmap[n], lv) for n in space_names if n in dmap}))
+
+    values = []
     if rd_loops:
         op = s.expr.op
         flags = _unroll_flags([l.extent for l in rd_loops], s.pragma_unroll)
-        acc = g.new(g.fr)
         mv = "b32" if g.ft == "f32" else "b64"
-        g(f"mov.{mv} {acc}, {g.fconst(0.0 if op == 'sum' else -math.inf)};")
+        accs = []
+        for _ in range(U):
+            acc = g.new(g.fr)
+            g(f"mov.{mv} {acc}, {g.fconst(0.0 if op == 'sum' else -math.inf)};")
+            accs.append(acc)
         body = s.expr.body
 
-        def rec(i, lv):
+        def rec(i, rlv):
             if i == len(rd_loops):
-                env2 = dict(env)
-                for n, d in s.index_map:
-                    if n not in space_names:
-                        env2[n] = dec(d, lv)
-                ex = Expr(g, lambda n: env2[n], k.reader(s, lambda n: env2[n]))
-                if op == "sum" and kind(body) == "Bin" and body.op == "mul":
-                    a, b = ex(body.lhs), ex(body.rhs)
-                    g(f"fma.rn.{g.ft} {acc}, {a}, {b}, {acc};")
-                else:
-                    v = ex(body)
-                    g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {acc}, {acc}, {v};")
+                for (guard, lv, env), acc in zip(pts, accs):
+                    env2 = dict(env)
+                    for n, d in s.index_map:
+                        if n not in space_names:
+                            env2[n] = dec(d, {**lv, **rlv})
+                    ex = Expr(g, lambda n, env2=env2: env2[n], k.reader(s, lambda n, env2=env2: env2[n]))
+                    ex.guard = guard
+                    if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                        a_, b_ = ex(body.lhs), ex(body.rhs)
+                        g(f"fma.rn.{g.ft} {acc}, {a_}, {b_}, {acc};")
+                    else:
+                        v = ex(body)
+                        g(f"{'add.rn' if op == 'sum' else 'max'}.{g.ft} {acc}, {acc}, {v};")
                 return
             l = rd_loops[i]
-            k.loop(l.extent, flags[i], lambda r: rec(i + 1, {**lv, l.id: r}))
-        rec(0, lv)
-        value = acc
+            k.loop(l.extent, flags[i], lambda r: rec(i + 1, {**rlv, l.id: r}))
+        rec(0, {})
+        values = accs
     else:
         expr = s.expr.body if kind(s.expr) == "Reduce" else s.expr
-        value = Expr(g, lambda n: env[n], k.reader(s, lambda n: env[n]))(expr)
-    k.epilogue(s, {n: env[n] for n in space_names}, value, mod.must_materialize(s))
+        for guard, lv, env in pts:
+            ex = Expr(g, lambda n, env=env: env[n], k.reader(s, lambda n, env=env: env[n]))
+            ex.guard = guard
+            values.append(ex(expr))
+    for (guard, lv, env), value in zip(pts, values):
+        k.store_guard = guard
+        k.epilogue(s, {n: env[n] for n in space_names}, value, mod.must_materialize(s))
+    k.store_guard = None
     g.pop()
-    g(f"add.s32 {pidx}, {pidx}, {grid * NAIVE_THREADS};")
+    g(f"add.s32 {pidx}, {pidx}, {U * step};")
     g(f"setp.lt.s32 {pe}, {pidx}, {total};")
     g(f"@{pe} bra {top};")
     g.label(done)
     args = _args(k, mod, s)
-    return k, Kernel(entry, grid, NAIVE_THREADS, 0, args, {"template": "naive", "stage": s.name, "points": total})
+    return k, Kernel(entry, grid, NAIVE_THREADS, 0, args, {"template": "naive", "stage": s.name, "points": total,
+                                                            "points_per_thread_step": U})
 
 
 def _args(k: _Kern, mod: _Mod, s) -> list:
