@@ -607,7 +607,10 @@ class _Kern:
         return "\n".join(head + decl + self.body + loads + g.lines + ["  ret;", "}"]) + "\n"
 
 
-NAIVE_POINTS = 4        # output points per thread per grid-stride step (loads in flight)
+# output points per thread per grid-stride step.  4 was measured on the golden
+# streams (tools/template_bench.py) with no gain over 1 (naive kernels are not
+# bound by loads in flight) and costs PTX size, i.e. compile time: 1.
+NAIVE_POINTS = int(os.environ.get("LT_NAIVE_POINTS", "1"))
 
 
 def _naive(mod: _Mod, s, entry: str) -> tuple:
@@ -621,7 +624,7 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
     total = 1
     for l in sp_loops:
         total *= l.extent
-    U = NAIVE_POINTS if "naive4" not in _OFF else 1
+    U = max(1, NAIVE_POINTS)
     if total + U * 148 * 16 * NAIVE_THREADS >= (1 << 31):
         raise Unsupported("index space exceeds 2^31")
     grid = max(1, min((total + NAIVE_THREADS * U - 1) // (NAIVE_THREADS * U), 148 * 16))
