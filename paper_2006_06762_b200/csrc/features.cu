@@ -313,19 +313,37 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
   }
 
   // working set inside each nest position (src/features.py:266-274)
+  // An iterator's interval at position pos depends only on which of ITS own loops
+  // sit inside pos (key = iter_mask & inside), so it is recomputed only when that
+  // key changes, and the working set only when some interval changed.
   double ws[MAX_NEST];
-  for (int pos = 0; pos < n_nest; ++pos) {
+  {
     Iv iv2[MAX_ITERS];
-    for (int it = 0; it < n_iter; ++it)
-      ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, iv2[it]);
+    unsigned long long seen[MAX_ITERS];
     double acc_ws = 0.0;
-    for (int v = 0; v < n_views; ++v) {
-      long long p = 1;
-      const int32_t* d = views[v].dims;
-      for (int k = 0; k < views[v].n_dims; ++k) { p *= hull_width(d, iv2); d = dim_next(d); }
-      acc_ws += (double)p * 4.0;
+    for (int pos = 0; pos < n_nest; ++pos) {
+      unsigned long long inside = 0;
+      for (int j = 0; j < n_loops; ++j)
+        if (loops[3 * j + 2] > pos) inside |= 1ULL << j;
+      bool changed = false;
+      for (int it = 0; it < n_iter; ++it) {
+        const unsigned long long key = iter_mask[it] & inside;
+        if (pos > 0 && key == seen[it]) continue;
+        ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, iv2[it]);
+        seen[it] = key;
+        changed = true;
+      }
+      if (changed) {
+        acc_ws = 0.0;
+        for (int v = 0; v < n_views; ++v) {
+          long long p = 1;
+          const int32_t* d = views[v].dims;
+          for (int k = 0; k < views[v].n_dims; ++k) { p *= hull_width(d, iv2); d = dim_next(d); }
+          acc_ws += (double)p * 4.0;
+        }
+      }
+      ws[pos] = acc_ws;
     }
-    ws[pos] = acc_ws;
   }
 
   // ---- row assembly (src/features.py:388-417) ----
