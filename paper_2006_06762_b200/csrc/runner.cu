@@ -8,8 +8,10 @@
 //   3. verifies every output against its fp64 ground-truth slot on the device:
 //      max |got - ref| / max(|ref|, 1e-30) (the reference's _check_outputs
 //      metric, src/machine.py:193-208) reduced to one float,
-//   4. re-runs the list r times between CUDA events on the task's stream, r chosen
-//      so the timed region lasts >= min_ms, and reports mean microseconds.
+//   4. re-runs the list r >= min_repeat times between CUDA events on the task's
+//      stream, r chosen so the timed region lasts >= min_ms, and reports mean
+//      microseconds (the runner passes min_repeat 1: the warm-up run carries
+//      first-launch costs and is never the measurement).
 // Launch failures (e.g. too many registers x threads) are statuses, not errors.
 
 #include <cuda.h>

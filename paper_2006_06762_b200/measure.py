@@ -251,7 +251,7 @@ class Runner:
 
     def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
                  min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0,
-                 min_repeat: int = 0, backend: str = "ptx", lower_workers: int | None = None):
+                 min_repeat: int = 1, backend: str = "ptx", lower_workers: int | None = None):
         self.lib = rt.load()
         self.device = device
         rt.check(self.lib.lt_set_device(device), "set device")
