@@ -35,6 +35,7 @@ from .state.expr import kind, reads
 
 
 LOOKAHEAD = 64      # statements between a shared-memory load and its first use
+FETCH_CHUNK = 8     # global loads in flight per thread in a rolled cooperative fetch
 # template switches (all on in production; LT_PTX_OFF=promote,plan,pad turns them off for A/B checks)
 _OFF = set(os.environ.get("LT_PTX_OFF", "").split(","))
 
@@ -902,19 +903,26 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     plain = sum(o["size"] for o in operands) * g.esz
     if plain > MAX_SMEM:
         raise LoweringError(f"shared memory {plain} bytes exceeds {MAX_SMEM}")
-    # innermost register level per space axis: unit-stride runs there allow
-    # vector shared loads when that dim is laid out innermost
-    last_s = [lv for lv in reg_levels if lv in inner] or reg_levels
+    # contiguous register runs: per space axis, the trailing inner register levels
+    # (S3 S4 for SSSRRSRS) are adjacent digits of the axis's mixed radix, so a
+    # thread's values along them are unit-stride when that dim is laid out
+    # innermost -> vector shared loads of up to 4 words
+    run_lvs = [lv for lv in inner if lv[0] == "S"]
+
+    def run_len(n):
+        r = 1
+        for lv in run_lvs:
+            r *= f(n, lv)
+        return r
     for o in operands:
         o["vec"], o["order"] = 1, list(range(len(o["hull"])))
-        if not last_s:
+        if not run_lvs:
             continue
-        lv4 = last_s[-1]
         for di, lin in enumerate(o["read"].index):
             for n, cc in lin.terms:
-                if n in T and cc == 1 and f(n, lv4) > 1 and o["off"][di] % 4 == 0 and \
+                if n in T and cc == 1 and run_len(n) > 1 and o["off"][di] % 4 == 0 and \
                         sum(1 for l2 in o["read"].index for n2, _ in l2.terms if n2 == n) == 1:
-                    w = 4 if f(n, lv4) % 4 == 0 else (2 if f(n, lv4) % 2 == 0 else 1)
+                    w = 4 if run_len(n) % 4 == 0 else (2 if run_len(n) % 2 == 0 else 1)
                     if w > o["vec"]:
                         o["vec"], o["vaxis"] = w, n
                         o["order"] = [d for d in range(len(o["hull"])) if d != di] + [di]
@@ -1134,10 +1142,18 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     else:
                         elem(Aff.reg(tid) + t * n_threads, not full and t == trips - 1)
             else:
-                def run(tv, o=o, full=full, elem=elem):
-                    elem(Aff.reg(tid) + tv.scale(n_threads), not full)
-                    fetch_store([items.pop()], sm)
-                k.loop(trips, False, run)
+                # long fetches: a rolled loop over chunks of FETCH_CHUNK trips, each
+                # chunk issuing all its global loads before its shared stores
+                n_ch = -(-trips // FETCH_CHUNK)
+
+                def run(tv, o=o, elem=elem):
+                    first = len(items)
+                    for j in range(FETCH_CHUNK):
+                        elem(Aff.reg(tid) + (tv.scale(FETCH_CHUNK) + j).scale(n_threads), True)
+                    chunk = items[first:]
+                    del items[first:]
+                    fetch_store(chunk, sm)
+                k.loop(n_ch, False, run)
         return items
 
     def fetch_store(items, buf):
@@ -1174,9 +1190,14 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         o["coef"], o["c0"] = coef, c0
         w = o["vec"]
         if w > 1:   # every run must start on a w-word boundary, or fall back to scalar loads
-            lv4 = ([lv for lv in reg_levels if lv in inner] or reg_levels)[-1]
-            ok = c0 % w == 0 and coef.get((o["vaxis"], lv4)) == 1 and f(o["vaxis"], lv4) % w == 0
-            ok = ok and all(c % w == 0 for kv, c in coef.items() if kv != (o["vaxis"], lv4))
+            va = o["vaxis"]
+            ok = c0 % w == 0 and run_len(va) % w == 0
+            stride = 1
+            for lv in reversed(run_lvs):       # run digits: unit-stride mixed radix
+                if f(va, lv) > 1:
+                    ok = ok and coef.get((va, lv)) == stride
+                stride *= f(va, lv)
+            ok = ok and all(c % w == 0 for kv, c in coef.items() if not (kv[0] == va and kv[1] in run_lvs))
             if not ok:
                 o["vec"] = 1
     op_of = {o["key"]: o for o in operands}
