@@ -36,6 +36,7 @@ from .state.expr import kind, reads
 
 LOOKAHEAD = 64      # statements between a shared-memory load and its first use
 FETCH_CHUNK = 8     # global loads in flight per thread in a rolled cooperative fetch
+ASYNC_MAX_TRIPS = 64  # cp.async staging: per-operand trips per thread (carry-free beyond 16)
 # template switches (all on in production; LT_PTX_OFF=promote,plan,pad turns them off for A/B checks)
 _OFF = set(os.environ.get("LT_PTX_OFF", "").split(","))
 
@@ -391,6 +392,23 @@ class _Kern:
         return flat
 
     def gload(self, name: str, idx: list, guard) -> str:
+        g = self.g
+        base, flat = self.gsource(name, idx)
+        key = ("gld", base, flat.key(), flat.const, guard)
+        hit = g.cached(key)
+        if hit:
+            return hit
+        rb, imm = g.gaddr(base, flat)
+        f = g.new(g.fr)
+        pred = f"@{guard} " if guard else ""
+        if guard:
+            g(f"mov.b{32 if g.ft == 'f32' else 64} {f}, 0;")
+        g(f"{pred}ld.global.nc.{g.ft} {f}, [{rb}+{imm}];")
+        return g.remember(key, f)
+
+    def gsource(self, name: str, idx: list) -> tuple:
+        """(pointer register, flat element Aff) of element `idx` of a global input,
+        through the packed physical layout when the State rewrote it."""
         g, m = self.g, self.m
         desc = m.layouts.get(name) if name not in m.live else None
         if desc is not None:
@@ -418,17 +436,7 @@ class _Kern:
                 m.buffers[name] = Buffer(name, m.shape(name), "input")
             base = self.param(name)
             flat = self.gflat(name, idx)
-        key = ("gld", base, flat.key(), flat.const, guard)
-        hit = g.cached(key)
-        if hit:
-            return hit
-        rb, imm = g.gaddr(base, flat)
-        f = g.new(g.fr)
-        pred = f"@{guard} " if guard else ""
-        if guard:
-            g(f"mov.b{32 if g.ft == 'f32' else 64} {f}, 0;")
-        g(f"{pred}ld.global.nc.{g.ft} {f}, [{rb}+{imm}];")
-        return g.remember(key, f)
+        return base, flat
 
     def gbase(self, name: str) -> str:
         """Pointer register of an unpacked global buffer (registers it as a parameter)."""
@@ -1052,11 +1060,18 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # emitted once before the staging loop
     fetch_plan: dict = {}
 
-    def prep_fetch():
+    def plannable(o, trips, long_ok):
+        """Hoisted per-trip addressing: always up to 16 trips; up to ASYNC_MAX_TRIPS
+        when the trip decomposition is carry-free (one base register + immediates)."""
+        if trips <= 16:
+            return True
+        return long_ok and trips <= ASYNC_MAX_TRIPS and carry_free_shifts(o, trips) is not None
+
+    def prep_fetch(long_ok=False):
         zero = lambda r: Aff.k(0)  # noqa: E731
         for oi, o in enumerate(operands):
             trips = -(-o["size"] // n_threads)
-            if trips > 16 or "plan" in _OFF:
+            if not plannable(o, trips, long_ok) or "plan" in _OFF:
                 continue
             full = o["size"] % n_threads == 0
             shifts = carry_free_shifts(o, trips)
@@ -1169,6 +1184,58 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 g.remember(key, a)
             pred = f"@{pt} " if pt else ""
             g(f"{pred}st.shared.{g.ft} [{a}+{sc * g.esz}], {v};")
+
+    def fetch_async(sdig, buf, pnext):
+        """One staging step as cp.async copies global -> shared (no register
+        round trip): every element of every operand, predicated on its tail
+        guard and on `pnext`; the caller commits the group."""
+        for oi, o in enumerate(operands):
+            r = o["read"]
+            base = operand_base(o, sdig)
+            zero_base = operand_base(o, lambda n: Aff.k(0))
+            trips = -(-o["size"] // n_threads)
+            for t in range(trips):
+                cs, tail, (sa, sc), ptr = fetch_plan[(oi, t)]
+                pt = pnext
+                if tail is not None:
+                    pt = tail
+                    if pnext is not None:
+                        pt = g.new("%p")
+                        g(f"and.pred {pt}, {tail}, {pnext};")
+                if ptr is None:             # packed layout: element address per stage
+                    gb, flat = k.gsource(r.buffer, [b_ + c for b_, c in zip(base, cs)])
+                    rb, imm = g.gaddr(gb, flat)
+                    emit_cp(sa, sc, buf, pt, rb, imm)
+                    continue
+                flat = k.gflat(r.buffer, [b_ + c for b_, c in zip(base, cs)])
+                inv = k.gflat(r.buffer, [b_ + c for b_, c in zip(zero_base, cs)])
+                off = flat + inv.scale(-1)
+                if off.terms:
+                    k2 = ("gptr@", ptr[0], off.key())
+                    rb = g.cached(k2)
+                    if rb is None:
+                        o_ = g.aff(off.runtime())
+                        w_ = g.new("%rd")
+                        g(f"mul.wide.s32 {w_}, {o_}, {g.esz};")
+                        rb = g.new("%rd")
+                        g(f"add.s64 {rb}, {ptr[0]}, {w_};")
+                        g.remember(k2, rb)
+                else:
+                    rb = ptr[0]
+                emit_cp(sa, sc, buf, pt, rb, flat.const * g.esz)
+
+    def emit_cp(sa, sc, buf, pt, rb, imm):
+        key = ("sst", sa, buf)
+        a = g.cached(key)
+        if a is None:
+            a = g.new("%r")
+            if sa is None:
+                g(f"mov.u32 {a}, {buf};")
+            else:
+                g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {buf};")
+            g.remember(key, a)
+        pred = f"@{pt} " if pt else ""
+        g(f"{pred}cp.async.ca.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], {g.esz};")
 
     # address coefficients: shared-memory word address of operand o as
     #   const0 + sum over local level digits (axis, level) of coef * digit
@@ -1380,10 +1447,53 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     for _, e in stage_axes:
         n_stage *= e
     trips_all = [-(-o["size"] // n_threads) for o in operands]
-    double = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
+    # asynchronous staging (cp.async, double-buffered): every operand a plain global
+    # read (no inline producer, no packed layout) with hoistable addressing
+    use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and
+                 all(o["read"].buffer not in attached_prod and plannable(o, t, True)
+                     for o, t in zip(operands, trips_all)))
+    double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
-    prep_fetch()
-    if not double:
+    prep_fetch(long_ok=use_async)
+    if use_async:
+        buf = total_words * g.esz
+        radices = [e for _, e in stage_axes]
+
+        def digits_of(treg):
+            ds = g.decompose(treg, radices)
+            m = {r: Aff.reg(d) for (r, _), d in zip(stage_axes, ds)}
+            return lambda r: m.get(r, Aff.k(0))
+        g.push()
+        fetch_async(lambda r: Aff.k(0), sm, None)
+        g.pop()
+        g("cp.async.commit_group;")
+        t = g.new("%r")
+        lab = g.new_label()
+        g(f"mov.s32 {t}, 0;")
+        g.label(lab)
+        g(".pragma \"nounroll\";")
+        g.push()
+        par, smb, nbuf, t1, pn = g.new("%r"), g.new("%r"), g.new("%r"), g.new("%r"), g.new("%p")
+        g(f"and.b32 {par}, {t}, 1;")
+        g(f"mad.lo.s32 {smb}, {par}, {buf}, {sm};")
+        g(f"xor.b32 {nbuf}, {par}, 1;")
+        g(f"mad.lo.s32 {nbuf}, {nbuf}, {buf}, {sm};")
+        g(f"add.s32 {t1}, {t}, 1;")
+        g(f"setp.lt.s32 {pn}, {t1}, {n_stage};")
+        fetch_async(digits_of(t1), nbuf, pn)       # next step's copies fly during this step
+        g("cp.async.commit_group;")
+        g("cp.async.wait_group 1;")                # this step's group has landed
+        g("bar.sync 0;")
+        compute(digits_of(t), smb)
+        g("bar.sync 0;")                           # the buffer is refilled next iteration
+        g.pop()
+        g(f"add.s32 {t}, {t}, 1;")
+        pl = g.new("%p")
+        g(f"setp.lt.s32 {pl}, {t}, {n_stage};")
+        g(f"@{pl} bra {lab};")
+        g("cp.async.wait_group 0;")
+        smem_bytes = 2 * buf
+    elif not double:
         def stage_rec(i, sd):
             if i == len(stage_axes):
                 sdig = lambda r, sd=sd: sd.get(r, Aff.k(0))  # noqa: E731
@@ -1481,7 +1591,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     info = {"template": "tiled", "stage": s.name, "structure": structure, "threads": n_threads,
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
             "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx",
-            "double_buffered": double, "acc_in_regs": acc_in_regs, "n_stage": n_stage}
+            "double_buffered": double or use_async, "async_copy": use_async, "acc_in_regs": acc_in_regs,
+            "n_stage": n_stage}
     return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
 
 
