@@ -1194,6 +1194,26 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             base = operand_base(o, sdig)
             zero_base = operand_base(o, lambda n: Aff.k(0))
             trips = -(-o["size"] // n_threads)
+            if (oi, 0) not in fetch_plan:
+                # no hoistable addressing: a rolled loop over chunks of trips, every
+                # element's coordinates decomposed in place (copies stay asynchronous)
+                def chunk(tv, o=o, r=r, base=base):
+                    for j in range(FETCH_CHUNK):
+                        er = g.aff(Aff.reg(tid) + (tv.scale(FETCH_CHUNK) + j).scale(n_threads))
+                        pt = g.new("%p")
+                        g(f"setp.lt.s32 {pt}, {er}, {o['size']};")
+                        if pnext is not None:
+                            g(f"and.pred {pt}, {pt}, {pnext};")
+                        cs = g.decompose(er, o["hull"])
+                        gb, flat = k.gsource(r.buffer, [b_ + Aff.reg(c) for b_, c in zip(base, cs)])
+                        rb, imm = g.gaddr(gb, flat)
+                        saddr = Aff.k(o["base_word"])
+                        for c, st_ in zip(cs, o["stride"]):
+                            saddr = saddr + Aff.reg(c, st_)
+                        emit_cp(g.aff(saddr.runtime()) if saddr.runtime().terms else None, saddr.const, buf, pt,
+                                rb, imm)
+                k.loop(-(-trips // FETCH_CHUNK), False, chunk)
+                continue
             for t in range(trips):
                 cs, tail, (sa, sc), ptr = fetch_plan[(oi, t)]
                 pt = pnext
@@ -1450,8 +1470,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # asynchronous staging (cp.async, double-buffered): every operand a plain global
     # read (no inline producer, no packed layout) with hoistable addressing
     use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and
-                 all(o["read"].buffer not in attached_prod and plannable(o, t, True)
-                     for o, t in zip(operands, trips_all)))
+                 all(o["read"].buffer not in attached_prod for o in operands))
     double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
     prep_fetch(long_ok=use_async)
