@@ -396,7 +396,7 @@ class Runner:
                 elif key in batch_keys:
                     job = ("dup", key)
                 else:
-                    job = self.submit(lo.source)
+                    job = self.submit(lo.source, PTX_SAFE_OPTS if lo.info.get("ptxas_opt") == "-O1" else None)
                     batch_keys[key] = job
                 q.put((i, p, lo, key, job))
         finally:
@@ -504,7 +504,8 @@ class Runner:
         if m.status != 0:
             rec.detail = "gpu: " + m.detail.decode(errors="replace")
             return
-        if not (rec.max_rel_err <= GPU_TOL) and lo.source.startswith(".version") and m.status == 0:
+        if not (rec.max_rel_err <= GPU_TOL) and lo.source.startswith(".version") and m.status == 0 and \
+                lo.info.get("ptxas_opt") != "-O1":
             m2 = self._remeasure_safe(lo, key, entries, ctx)
             if m2 is not None:
                 m = m2

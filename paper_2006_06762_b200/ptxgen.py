@@ -36,6 +36,7 @@ from .state.expr import kind, reads
 
 LOOKAHEAD = 64      # statements between a shared-memory load and its first use
 FETCH_CHUNK = 8     # global loads in flight per thread in a rolled cooperative fetch
+SPILL_MARGIN = 24    # registers beyond the accumulator tile a tiled kernel needs
 ASYNC_MAX_TRIPS = 64  # cp.async staging: per-operand trips per thread (carry-free beyond 16)
 # template switches (all on in production; LT_PTX_OFF=promote,plan,pad turns them off for A/B checks)
 _OFF = set(os.environ.get("LT_PTX_OFF", "").split(","))
@@ -1657,5 +1658,14 @@ def lower_ptx(p, dtype: str = "float") -> Lowered:
             mod.buffers[name] = Buffer(name, tuple(e for _, e in st.space),
                                        "output" if name in p.dag.outputs else "temp")
     head = ".version 8.7\n.target sm_100a\n.address_size 64\n.extern .shared .align 16 .b8 smem_[];\n"
-    return Lowered(head + "\n".join(texts), kernels, mod.buffers, list(p.dag.outputs),
-                   {"kernels": [k.info for k in kernels], "backend": "ptx"})
+    info = {"kernels": [k.info for k in kernels], "backend": "ptx"}
+    # ptxas -O3 has miscompiled kernels whose register tile overflows the register
+    # file (wrong values, out-of-range shared addresses, kernel faults; correct at
+    # -O1 and through NVRTC): such modules are assembled at -O1 up front
+    for kk in kernels:
+        ki = kk.info
+        if ki.get("template") == "tiled" and ki.get("acc_in_regs") and \
+                ki["acc"] + SPILL_MARGIN > min(255, 65536 // ki["threads"]):
+            info["ptxas_opt"] = "-O1"
+            ki["ptxas"] = "-O1 (register tile exceeds the register file)"
+    return Lowered(head + "\n".join(texts), kernels, mod.buffers, list(p.dag.outputs), info)
