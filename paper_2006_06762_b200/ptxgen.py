@@ -1470,8 +1470,11 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     trips_all = [-(-o["size"] // n_threads) for o in operands]
     # asynchronous staging (cp.async, double-buffered): every operand a plain global
     # read (no inline producer, no packed layout) with hoistable addressing
+    # ... and only where the second buffer does not cost resident blocks (smem-bound
+    # tilings lose more latency hiding to halved occupancy than they gain)
     use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and
-                 all(o["read"].buffer not in attached_prod for o in operands))
+                 all(o["read"].buffer not in attached_prod for o in operands) and
+                 _blocks_per_sm(n_threads, n_acc, 2 * smem_bytes) >= _blocks_per_sm(n_threads, n_acc, smem_bytes))
     double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
     prep_fetch(long_ok=use_async)
@@ -1614,6 +1617,16 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             "double_buffered": double or use_async, "async_copy": use_async, "acc_in_regs": acc_in_regs,
             "n_stage": n_stage}
     return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
+
+
+def _blocks_per_sm(threads: int, n_acc: int, smem: int) -> int:
+    """Resident blocks per SM (B200: 2048 threads, 64K registers, 228 KB shared
+    memory with 1 KB reserved per block, 32 blocks), registers estimated as the
+    accumulator tile plus SPILL_MARGIN."""
+    regs = min(255, -(-(n_acc + SPILL_MARGIN) // 8) * 8)
+    by_regs = 65536 // max(1, threads * regs)
+    by_smem = (228 * 1024) // (smem + 1024) if smem else 32
+    return max(0, min(32, 2048 // threads, by_regs, by_smem))
 
 
 def _local_addr(g: Ptx, ab: str, ai: Aff) -> tuple:
