@@ -1470,11 +1470,14 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     trips_all = [-(-o["size"] // n_threads) for o in operands]
     # asynchronous staging (cp.async, double-buffered): every operand a plain global
     # read (no inline producer, no packed layout) with hoistable addressing
-    # ... and only where the second buffer does not cost resident blocks (smem-bound
-    # tilings lose more latency hiding to halved occupancy than they gain)
+    # ... and only where the second buffer keeps the SM busy: the same resident
+    # blocks, or still >= 4 resident warps (measured on the golden streams: tilings
+    # pushed below that lose more latency hiding than the overlap wins)
+    occ1 = _blocks_per_sm(n_threads, n_acc, smem_bytes)
+    occ2 = _blocks_per_sm(n_threads, n_acc, 2 * smem_bytes)
     use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and
                  all(o["read"].buffer not in attached_prod for o in operands) and
-                 _blocks_per_sm(n_threads, n_acc, 2 * smem_bytes) >= _blocks_per_sm(n_threads, n_acc, smem_bytes))
+                 (occ2 >= occ1 or occ2 * -(-n_threads // 32) >= 4))
     double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
     prep_fetch(long_ok=use_async)
