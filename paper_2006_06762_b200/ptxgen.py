@@ -1475,7 +1475,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # pushed below that lose more latency hiding than the overlap wins)
     occ1 = _blocks_per_sm(n_threads, n_acc, smem_bytes)
     occ2 = _blocks_per_sm(n_threads, n_acc, 2 * smem_bytes)
-    use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and
+    spill_heavy = acc_in_regs and n_acc + SPILL_MARGIN > min(255, 65536 // n_threads)
+    use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and not spill_heavy and
                  all(o["read"].buffer not in attached_prod for o in operands) and
                  (occ2 >= occ1 or occ2 * -(-n_threads // 32) >= 4))
     double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
@@ -1680,7 +1681,7 @@ def lower_ptx(p, dtype: str = "float") -> Lowered:
     # -O1 and through NVRTC): such modules are assembled at -O1 up front
     for kk in kernels:
         ki = kk.info
-        if ki.get("template") == "tiled" and ki.get("acc_in_regs") and \
+        if "o1guard" not in _OFF and ki.get("template") == "tiled" and ki.get("acc_in_regs") and \
                 ki["acc"] + SPILL_MARGIN > min(255, 65536 // ki["threads"]):
             info["ptxas_opt"] = "-O1"
             ki["ptxas"] = "-O1 (register tile exceeds the register file)"
