@@ -35,11 +35,11 @@ from .state.expr import kind, reads
 
 
 LOOKAHEAD = 64      # statements between a shared-memory load and its first use
-FETCH_CHUNK = 8     # global loads in flight per thread in a rolled cooperative fetch
 SPILL_MARGIN = 24    # registers beyond the accumulator tile a tiled kernel needs
 ASYNC_MAX_TRIPS = 64  # cp.async staging: per-operand trips per thread (carry-free beyond 16)
 # template switches (all on in production; LT_PTX_OFF=promote,plan,pad turns them off for A/B checks)
 _OFF = set(os.environ.get("LT_PTX_OFF", "").split(","))
+FETCH_CHUNK = 1 if "chunk" in _OFF else 8   # loads in flight per thread in a rolled cooperative fetch
 
 
 class Unsupported(Exception):
@@ -917,6 +917,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # thread's values along them are unit-stride when that dim is laid out
     # innermost -> vector shared loads of up to 4 words
     run_lvs = [lv for lv in inner if lv[0] == "S"]
+    if "vrun" in _OFF:
+        run_lvs = run_lvs[-1:]
 
     def run_len(n):
         r = 1
