@@ -767,7 +767,7 @@ def _smem_strides(hull: list, lane_coords, order=None, step: int = 1, store_coor
             best = (cand, st, m)
         if deg == 1 and sdeg == 1:
             break
-    return best[1], best[2]
+    return best[1], best[2], best[0][0]
 
 
 def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
@@ -925,6 +925,22 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         for lv in run_lvs:
             r *= f(n, lv)
         return r
+    def others_aligned(lin, n, w):
+        """Every other iterator digit in this index dim moves by a multiple of w
+        words when the dim is laid out innermost (else the runs would straddle
+        vector boundaries and the layout change would buy nothing)."""
+        for n2, c2 in lin.terms:
+            if n2 == n:
+                continue
+            kind_ = "S" if n2 in T else "R"
+            for kk in range(1, n_s if kind_ == "S" else n_r):
+                if f(n2, (kind_, kk)) > 1:
+                    m = 1
+                    for k2 in range(kk + 1, n_s if kind_ == "S" else n_r):
+                        m *= factors[n2][k2]
+                    if (c2 * m) % w:
+                        return False
+        return True
     for o in operands:
         o["vec"], o["order"] = 1, list(range(len(o["hull"])))
         if not run_lvs:
@@ -934,7 +950,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 if n in T and cc == 1 and run_len(n) > 1 and o["off"][di] % 4 == 0 and \
                         sum(1 for l2 in o["read"].index for n2, _ in l2.terms if n2 == n) == 1:
                     w = 4 if run_len(n) % 4 == 0 else (2 if run_len(n) % 2 == 0 else 1)
-                    if w > o["vec"]:
+                    if w > o["vec"] and others_aligned(lin, n, w):
                         o["vec"], o["vaxis"] = w, n
                         o["order"] = [d for d in range(len(o["hull"])) if d != di] + [di]
     total_words = 0
@@ -960,8 +976,15 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 x //= h
             if x == 0:
                 scoords.append(c[::-1])
-        o["stride"], o["words"] = _smem_strides(o["hull"], coords, o["order"], o["vec"],
-                                                None if "pad" in _OFF else scoords)
+        sc_ = None if "pad" in _OFF else scoords
+        o["stride"], o["words"], deg = _smem_strides(o["hull"], coords, o["order"], o["vec"], sc_)
+        if o["vec"] > 1:
+            # a vector layout is kept only if its compute-side wavefronts per
+            # element (conflict degree / vector width) beat the natural layout's
+            st1, w1, deg1 = _smem_strides(o["hull"], coords, list(range(len(o["hull"]))), 1, sc_)
+            if deg1 < deg / o["vec"] or (deg1 == deg / o["vec"] and w1 < o["words"]):
+                o["stride"], o["words"], o["vec"] = st1, w1, 1
+                o["order"] = list(range(len(o["hull"])))
         total_words = -(-total_words // 4) * 4          # 16-byte aligned operand bases
         o["base_word"] = total_words
         total_words += o["words"]
