@@ -8,6 +8,9 @@
                       with every tree fitted on the GPU (`csrc/gbdt.cu`);
                       `install(..., gpu_train=False)` keeps the reference's own
                       `train` and wraps its result as `GpuCostModel`;
+* `cli.cmd_replay` -> `replay.cmd_replay` (status parity exact, costs within a
+                      tolerance, device recorded) and tune-log headers gain a
+                      `runner` block (device, cost unit µs);
 * `evolve`         -> `evolve_batched`: the reference's evolution loop
                       (`src/evolve.py:442-502`) verbatim in its random-number use,
                       except that each population is scored with one
@@ -31,6 +34,7 @@ import numpy as np
 
 from .measure import measure_batch
 from .model import GpuCostModel
+from .replay import cmd_replay
 
 
 def make_evolve_batched(ev):
@@ -139,6 +143,18 @@ def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True) -> dict
             return gbdt.train(records, hyper)
         return GpuCostModel.wrap(ref_train(records, hyper) if hyper is not None else ref_train(records))
 
+    logio = importlib.import_module(loomtune.__name__ + ".logio")
+    orig["cli.cmd_replay"] = cli.cmd_replay
+    orig["logio.LogWriter.write"] = logio.LogWriter.write
+    ref_write = logio.LogWriter.write
+
+    def write(self, record):            # header records name the B200 runner (cost unit µs)
+        if record.get("kind") == "header" and "runner" not in record:
+            from .replay import runner_header
+            record = {**record, "runner": runner_header()}
+        return ref_write(self, record)
+    logio.LogWriter.write = write
+    cli.cmd_replay = cmd_replay         # wall-clock replay
     sched.measure_batch = measure_batch
     cli.measure_batch = measure_batch
     sched.train = train
@@ -157,3 +173,6 @@ def uninstall(loomtune, orig: dict) -> None:
     sched.evolve = orig["evolve"]
     cli.measure_batch = orig["cli.measure_batch"]
     sched.sample_program = orig["sample_program"]
+    if "cli.cmd_replay" in orig:
+        cli.cmd_replay = orig["cli.cmd_replay"]
+        importlib.import_module(loomtune.__name__ + ".logio").LogWriter.write = orig["logio.LogWriter.write"]

@@ -51,13 +51,19 @@ def test_install_rebinds_and_restores():
     from paper_2006_06762_b200 import integrate, measure
     import importlib
     sched, cli = importlib.import_module("loomtune.sched"), importlib.import_module("loomtune.cli")
+    from paper_2006_06762_b200 import replay
+    logio = importlib.import_module("loomtune.logio")
     orig = integrate.install(LT)
     try:
         assert sched.measure_batch is measure.measure_batch
         assert cli.measure_batch is measure.measure_batch
+        assert cli.cmd_replay is replay.cmd_replay
+        assert logio.LogWriter.write is not orig["logio.LogWriter.write"]
     finally:
         integrate.uninstall(LT, orig)
     assert sched.measure_batch is orig["measure_batch"]
+    assert cli.cmd_replay is orig["cli.cmd_replay"]
+    assert logio.LogWriter.write is orig["logio.LogWriter.write"]
 
 
 @pytest.mark.gpu
