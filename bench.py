@@ -280,7 +280,8 @@ def main() -> None:
 
     workers = max(1, cores // world - (1 if world == 1 else 0))
     cache = tempfile.mkdtemp(prefix="lt_cubin_")     # empty: every candidate really compiles
-    runner = measure.configure(device=local, workers=workers, cache_dir=cache)
+    runner = measure.configure(device=local, workers=workers, cache_dir=cache,
+                               lower_workers=max(1, min(8, cores // (2 * world))))
     runner.context(dag, 0)                             # inputs + fp64 ground truth resident
 
     B = args.batch

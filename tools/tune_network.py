@@ -51,7 +51,8 @@ def main() -> None:
         dist.init_process_group("nccl", init_method="env://")
         torch.cuda.set_device(local)
     runner = measure.configure(device=local, cache_dir="",
-                               workers=max(1, (os.cpu_count() or 2) // world - (1 if world == 1 else 0)))
+                               workers=max(1, (os.cpu_count() or 2) // world - (1 if world == 1 else 0)),
+                               lower_workers=max(1, min(8, (os.cpu_count() or 2) // (2 * world))))
     sched = importlib.import_module("loomtune.sched")
     orig = integrate.install(LT, gpu_sampler=bool(opt.get("--gpu-sampler")))
     if world > 1:
