@@ -301,6 +301,7 @@ def main() -> None:
 
     all_recs = []
     launch_log = []
+    refresh_s = []
 
     l2_flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")     # 256 MB > 126 MB L2
 
@@ -313,8 +314,10 @@ def main() -> None:
         for ps in progs:
             l2_flush.zero_()                   # 256 MB write: no step starts with a warm L2
             if fresh_ctx:   # e2e: inputs re-uploaded and ground truth recomputed inside the region
+                t_r = time.perf_counter()
                 for c in runner.ctx.values():
                     c.refresh()
+                refresh_s.append(time.perf_counter() - t_r)
             res = sharded_measure(ps)          # NCCL all_gather of (status, cost) records
             all_recs.append(res)
             launch_log.append(list(runner.last_records))
@@ -398,6 +401,8 @@ def main() -> None:
                          "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU"},
             "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
                     "d2h_bytes_per_step": int(d2h_step),
+                    "refresh_ms_per_step": 1e3 * sum(refresh_s) / max(1, len(refresh_s)),
+                    "ms_per_step": e2e_ms / args.steps,
                     "note": "measure_batch on host Programs; every step re-uploads the DAG's input tensors "
                             "(fp32+fp64, pageable) and recomputes the fp64 ground truth on the device; cubins "
                             "H2D; per-candidate error words D2H"},
