@@ -33,29 +33,12 @@ constexpr int MAX_STACK = 48;
 
 struct Iv { long long lo, hi; };
 
-// Python floor division / modulo.  Operands almost always fit 32 bits, where the
-// hardware sequence is several times shorter than the 64-bit division routine.
-__device__ __forceinline__ bool fits32(long long a, long long c) {
-  return a > -2147483648LL && a <= 2147483647LL && c > 0 && c <= 2147483647LL;
-}
 __device__ __forceinline__ long long fdiv(long long a, long long c) {
-  if (fits32(a, c)) {
-    const int ai = (int)a, ci = (int)c;
-    int q = ai / ci;
-    if ((ai % ci != 0) && (ai < 0)) --q;
-    return q;
-  }
   long long q = a / c;
   if ((a % c != 0) && ((a < 0) != (c < 0))) --q;
   return q;
 }
 __device__ __forceinline__ long long fmod_(long long a, long long c) {
-  if (fits32(a, c)) {
-    const int ai = (int)a, ci = (int)c;
-    int r = ai % ci;
-    if (r != 0 && r < 0) r += ci;
-    return r;
-  }
   long long r = a % c;
   if (r != 0 && ((r < 0) != (c < 0))) r += c;
   return r;
