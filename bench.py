@@ -412,6 +412,8 @@ def main() -> None:
                              "kernels": (best_rec.info.get("kernels") if best_rec else None)},
             "compile": {"compiled": stats["compiled"], "cache_hits": stats["cache_hits"],
                         "recompiled_O1": stats.get("recompiled", 0),
+                        "kernels_compiled": stats.get("kernels_compiled", 0),
+                        "kernels_shared": stats.get("kernels_shared", 0),
                         "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
             "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s")},
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

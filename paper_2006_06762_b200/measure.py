@@ -226,6 +226,23 @@ class _DagContext:
         return out
 
 
+def _modules_of(lo: Lowered) -> list:
+    """[(entries, module source, compile options)]: PTX candidates compile one
+    module per kernel, so a kernel shared by many candidates (a materialised
+    padding stage, an unchanged consumer) is assembled once; CUDA C candidates
+    stay one NVRTC module."""
+    if not lo.source.startswith(".version"):
+        return [([k.entry for k in lo.kernels], lo.source, None)]
+    head, _, rest = lo.source.partition(".visible .entry ")
+    bodies = [".visible .entry " + b for b in rest.split(".visible .entry ")]
+    out = []
+    for k, body in zip(lo.kernels, bodies):
+        if not body.startswith(f".visible .entry {k.entry}("):
+            raise LoweringError(f"module split mismatch at {k.entry}")
+        out.append(([k.entry], head + body, PTX_SAFE_OPTS if k.info.get("ptxas") else None))
+    return out
+
+
 def _lower_one(p, backend: str):
     """validate + lower one State (runs in a lowering worker process).
     Returns (kind, payload, seconds): ("bad", detail) | ("err", detail) | ("ok", Lowered)."""
@@ -274,6 +291,7 @@ class Runner:
         self.failed_keys: dict = {}
         self._drain_error = None
         self.stats = {"compiled": 0, "recompiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0,
+                      "kernels_compiled": 0, "kernels_shared": 0,
                       "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0}
         self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
@@ -394,16 +412,21 @@ class Runner:
                 recs[i].info = lo.info
                 key = hashlib.sha1(lo.source.encode()).hexdigest()
                 recs[i].key = key
-                with self.mod_lock:
-                    loaded = key in self.modules
-                if loaded:
-                    job = None
-                elif key in batch_keys:
-                    job = ("dup", key)
-                else:
-                    job = self.submit(lo.source, PTX_SAFE_OPTS if lo.info.get("ptxas_opt") == "-O1" else None)
-                    batch_keys[key] = job
-                q.put((i, p, lo, key, job))
+                parts = []
+                for ents, text, opts in _modules_of(lo):
+                    kkey = hashlib.sha1((opts or "") .encode() + text.encode()).hexdigest()
+                    with self.mod_lock:
+                        loaded = kkey in self.modules
+                    if loaded:
+                        parts.append((ents, kkey, None))
+                    elif kkey in batch_keys:                 # same kernel in another candidate
+                        parts.append((ents, kkey, ("dup", kkey)))
+                        self.stats["kernels_shared"] += 1
+                    else:
+                        job = self.submit(text, opts)
+                        batch_keys[kkey] = job
+                        parts.append((ents, kkey, job))
+                q.put((i, p, lo, key, parts))
         finally:
             q.put(None)
             worker.join()
@@ -437,13 +460,16 @@ class Runner:
                 yield i, p, _lower_one(p, self.backend)
 
     def _ready(self, item) -> bool:
-        job = item[4]
-        if job is None:
-            return True
-        if isinstance(job, tuple):
-            with self.mod_lock:
-                return job[1] in self.modules or job[1] in self.failed_keys
-        return self.lib.lt_compile_ready(job) != 0
+        for _, kkey, job in item[4]:
+            if job is None:
+                continue
+            if isinstance(job, tuple):
+                with self.mod_lock:
+                    if not (kkey in self.modules or kkey in self.failed_keys):
+                        return False
+            elif self.lib.lt_compile_ready(job) == 0:
+                return False
+        return True
 
     def _drain(self, q, recs, seed) -> None:
         waiting, closed = [], False
@@ -474,29 +500,33 @@ class Runner:
                     closed = True
 
     def _measure_one(self, item, recs, seed) -> None:
-        i, p, lo, key, job = item
+        i, p, lo, key, parts = item
         rec = recs[i]
         entries = [k.entry for k in lo.kernels]
-        if job is None or isinstance(job, tuple):
-            with self.mod_lock:
-                if key in self.failed_keys:
-                    rec.detail = self.failed_keys[key]
-                    return
-            funcs = self.load(key, b"", entries)
-            rec.cache_hit = True
-        else:
+        funcs, compiled, rec.cache_hit = [], False, True
+        for ents, kkey, job in parts:
+            if job is None or isinstance(job, tuple):
+                with self.mod_lock:
+                    if kkey in self.failed_keys:
+                        rec.detail = self.failed_keys[kkey]
+                        return
+                funcs += self.load(kkey, b"", ents)
+                continue
             st, secs, hit, data = self.collect(job)
-            rec.compile_s, rec.cache_hit = secs, hit
+            rec.compile_s += secs
+            rec.cache_hit = rec.cache_hit and hit
+            compiled = compiled or not hit
             self.stats["compile_s"] += secs
-            self.stats["cache_hits" if hit else "compiled"] += 1
+            self.stats["kernels_compiled"] += 0 if hit else 1
             if st != 0:
                 rec.detail = "gpu: compile failed: " + data.decode(errors="replace").strip()[:300]
                 with self.mod_lock:
-                    self.failed_keys[key] = rec.detail
+                    self.failed_keys[kkey] = rec.detail
                 return
             t0 = time.perf_counter()
-            funcs = self.load(key, data, entries)
+            funcs += self.load(kkey, data, ents)
             self.stats["load_s"] += time.perf_counter() - t0
+        self.stats["compiled" if compiled else "cache_hits"] += 1
         ctx = self.context(p.dag, seed)
         if _TRACE:
             print(f"[lt trace] measuring #{i} {key[:12]} {[k.info.get('template') for k in lo.kernels]}",
