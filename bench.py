@@ -257,6 +257,8 @@ def main() -> None:
     ap.add_argument("--cpu-seconds", type=float, default=30.0,
                     help="per-sample cap on a reference candidate's CPU time (truncated ones count their time)")
     ap.add_argument("--no-scoring", action="store_true")
+    ap.add_argument("--compile-workers", type=int, default=0, help="ptxas worker processes per rank (0: auto)")
+    ap.add_argument("--lower-workers", type=int, default=0, help="lowering processes per rank (0: auto)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -303,8 +305,10 @@ def main() -> None:
 
     workers = max(1, cores // world - (1 if world == 1 else 0))
     cache = tempfile.mkdtemp(prefix="lt_cubin_")     # empty: every candidate really compiles
+    if args.compile_workers:
+        workers = args.compile_workers
     runner = measure.configure(device=local, workers=workers, cache_dir=cache,
-                               lower_workers=max(1, min(8, cores // (2 * world))))
+                               lower_workers=args.lower_workers or max(1, min(8, cores // (2 * world))))
     runner.context(dag, 0)                             # inputs + fp64 ground truth resident
 
     B = args.batch
