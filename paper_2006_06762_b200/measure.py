@@ -405,7 +405,12 @@ class Runner:
         worker.start()
         batch_keys: dict = {}
         try:
-            for i, p, (kind_, payload, secs) in self._lowered(programs):
+            # all lowerings first (milliseconds each, in parallel), then compile jobs in
+            # decreasing source size: the longest ptxas runs start first, which shortens
+            # the batch's tail (longest-processing-time-first scheduling)
+            lowered = list(self._lowered(programs))
+            lowered.sort(key=lambda x: -len(x[2][1].source) if x[2][0] == "ok" else 0)
+            for i, p, (kind_, payload, secs) in lowered:
                 recs[i].lower_s = secs
                 self.stats["lower_s"] += secs
                 if kind_ != "ok":
