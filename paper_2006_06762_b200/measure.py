@@ -283,6 +283,7 @@ class Runner:
         self.workers = workers or max(1, (os.cpu_count() or 2) - 1)
         self.cache_dir = cache_dir if cache_dir is not None else os.environ.get(
             "LT_CUBIN_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "loomtune_b200", "cubin"))
+        self.compile_timeout = compile_timeout
         rt.check(self.lib.lt_pool_start(self.workers, self.cache_dir.encode() if self.cache_dir else None,
                                         compile_timeout), "compile pool")
         self.min_ms, self.max_repeat, self.min_repeat = min_ms, max_repeat, min_repeat
@@ -312,6 +313,19 @@ class Runner:
             from concurrent.futures import ProcessPoolExecutor
             self._lpool = ProcessPoolExecutor(self.lower_workers, mp_context=mp.get_context("spawn"))
         return self._lpool
+
+    def forget_compiled(self, cache_dir: str) -> None:
+        """Drop every compiled module and restart the compile pool on `cache_dir`
+        (benchmarks re-measuring the same States from scratch)."""
+        with self.mod_lock:
+            for m, _ in self.modules.values():
+                self.lib.lt_module_unload(m)
+            self.modules.clear()
+            self.failed_keys.clear()
+        self.lib.lt_pool_stop()
+        self.cache_dir = cache_dir
+        rt.check(self.lib.lt_pool_start(self.workers, cache_dir.encode() if cache_dir else None,
+                                        self.compile_timeout), "compile pool")
 
     def close(self):
         if self._lpool is not None:
