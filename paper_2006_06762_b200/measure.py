@@ -140,6 +140,7 @@ class _DagContext:
         # fp64 ground truth, computed once on the device from the fp64 inputs
         ref = reference_lowering(dag)
         funcs = runner.compile_and_load([ref.source], [[k.entry for k in ref.kernels]])[0]
+        runner.pinned.add(hashlib.sha1(ref.source.encode()).hexdigest())
         if isinstance(funcs, str):
             raise rt.NativeError(f"ground-truth kernel failed to compile: {funcs}")
         for name, b in ref.buffers.items():
@@ -291,6 +292,7 @@ class Runner:
         self.ctx: dict = {}
         self._dag_keys: dict = {}          # (id(dag), seed) -> (dag, content key)
         self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
+        self.pinned: set = set()                      # ground-truth modules (held by DAG contexts)
         self.mod_lock = threading.Lock()
         self.failed_keys: dict = {}
         self._drain_error = None
@@ -318,9 +320,8 @@ class Runner:
         """Drop every compiled module and restart the compile pool on `cache_dir`
         (benchmarks re-measuring the same States from scratch)."""
         with self.mod_lock:
-            for m, _ in self.modules.values():
-                self.lib.lt_module_unload(m)
-            self.modules.clear()
+            for k in [k for k in self.modules if k not in self.pinned]:
+                self.lib.lt_module_unload(self.modules.pop(k)[0])
             self.failed_keys.clear()
         self.lib.lt_pool_stop()
         self.cache_dir = cache_dir
@@ -390,8 +391,11 @@ class Runner:
             funcs.append(f)
         with self.mod_lock:
             self.modules[key] = (m, funcs)
-            while len(self.modules) > 512:
-                _, (old, _) = self.modules.popitem(last=False)
+            while len(self.modules) > 512:          # LRU, never the ground-truth modules
+                victim = next((k for k in self.modules if k not in self.pinned), None)
+                if victim is None:
+                    break
+                old, _ = self.modules.pop(victim)
                 self.lib.lt_module_unload(old)
         return funcs
 
