@@ -297,8 +297,12 @@ void Pool::loop() {
       for (auto& w : workers_) {
         if (w.job || queue_.empty()) continue;
         if (w.pid < 0 && spawn(w)) continue;
-        int64_t id = queue_.front();
-        queue_.pop_front();
+        // longest job first (source size ~ ptxas time): shortens a batch's tail
+        auto best = queue_.begin();
+        for (auto it = queue_.begin(); it != queue_.end(); ++it)
+          if (jobs_[*it].src.size() > jobs_[*best].src.size()) best = it;
+        int64_t id = *best;
+        queue_.erase(best);
         Job& j = jobs_[id];
         j.state = 1;
         j.started = std::chrono::steady_clock::now();

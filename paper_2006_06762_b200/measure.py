@@ -423,11 +423,12 @@ class Runner:
         worker.start()
         batch_keys: dict = {}
         try:
-            # all lowerings first (milliseconds each, in parallel), then compile jobs in
-            # decreasing source size: the longest ptxas runs start first, which shortens
-            # the batch's tail (longest-processing-time-first scheduling)
-            lowered = list(self._lowered(programs))
-            lowered.sort(key=lambda x: -len(x[2][1].source) if x[2][0] == "ok" else 0)
+            # compile jobs are submitted as lowerings finish; the pool hands the
+            # largest pending source to each free worker (longest-processing-time
+            # first), which shortens the batch's tail
+            lowered = self._lowered(programs)
+            if os.environ.get("LT_LOWER_ALL"):
+                lowered = sorted(lowered, key=lambda x: -len(x[2][1].source) if x[2][0] == "ok" else 0)
             for i, p, (kind_, payload, secs) in lowered:
                 recs[i].lower_s = secs
                 self.stats["lower_s"] += secs
