@@ -190,7 +190,7 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
 #define O(k) out[(int64_t)(k) * ld_col]
 
   const int n_nest = r[0], own_start = r[1], n_loops = r[2], n_iter = r[3], n_views = r[4];
-  const int unroll = r[5], n_live = r[6], has_reduce = r[7];
+  const int unroll = r[5], n_live = r[6], has_reduce = r[7] & 1, gpu_feats = r[7] & 2;
   const int32_t* ops = r + 8;
   const int n_nodes = r[17];
   if (n_nest > MAX_NEST || n_loops > MAX_LOOPS || n_iter > MAX_ITERS || n_views > MAX_VIEWS) {
@@ -375,7 +375,12 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
   }
   annotation_block(nest, n_nest, 1, b);
   for (int k = 0; k < 11; ++k) W(40 + k, b[k]);
-  for (int k = 51; k < 59; ++k) O(k) = 0.0;
+  if (gpu_feats) {          // opt-in: the kernel binding the encoder appended (8 trailing words)
+    const int32_t* gw = words + stmt_off[s + 1] - 8;
+    for (int k = 0; k < 8; ++k) W(51 + k, (double)gw[k]);
+  } else {
+    for (int k = 51; k < 59; ++k) O(k) = 0.0;     // the reference leaves the gpu_* slots zero
+  }
   if (n_nest == 0 || ops_total == 0) {
     for (int k = 59; k < 69; ++k) O(k) = 0.0;
   } else {

@@ -92,9 +92,12 @@ def _nest_above(smap: dict, s) -> list:
     return _nest_above(smap, t) + list(t.loops[: ids.index(lid) + 1])
 
 
-def encode_program(p, out: list, ops_cache: dict) -> int:
+def encode_program(p, out: list, ops_cache: dict, gpu_features: bool = False) -> int:
     """Append one record per live statement of `p` to `out` (a list of int
-    lists); returns the number of statements."""
+    lists); returns the number of statements.  gpu_features: flag the record
+    (has_reduce bit 1) and append the statement's kernel binding (blockIdx.x,
+    blockIdx.y, blockIdx.z, threadIdx.x, threadIdx.y, threadIdx.z, vthread,
+    shared bytes) as 8 trailing words; the kernel fills the gpu_* slots from them."""
     smap = _stage_map(p)
     layouts = dict(p.layouts)
     live = [s for s in p.stages if not s.inlined]
@@ -163,7 +166,7 @@ def encode_program(p, out: list, ops_cache: dict) -> int:
         rank = {b: r for r, b in enumerate(sorted(order))}
 
         rec = [len(nest), len(above), len(s.loops), len(iter_tab) // 2, len(order),
-               int(s.pragma_unroll), len(live), 1 if s.reduce else 0]
+               int(s.pragma_unroll), len(live), (1 if s.reduce else 0) | (2 if gpu_features else 0)]
         rec += _ops(s.expr, ops_cache)
         rec.append(len(nodes) // 2)
         for l in nest:
@@ -180,17 +183,21 @@ def encode_program(p, out: list, ops_cache: dict) -> int:
                 rec += (int(size), st, pext, int(const), len(terms))
                 for it, c in terms:
                     rec += (it, int(c))
+        if gpu_features:
+            from .lower import gpu_binding
+            nb, nt, nv, smem = gpu_binding(p, s)
+            rec += (min(nb, 2 ** 31 - 1), 1, 1, nt, 1, 1, nv, smem)
         out.append(rec)
     return len(live)
 
 
-def encode_batch(programs) -> tuple:
+def encode_batch(programs, gpu_features: bool = False) -> tuple:
     """-> (words int32[], stmt_offsets int64[n_stmt+1], prog_row_offsets int64[n_prog+1])."""
     recs: list = []
     prog_off = [0]
     cache: dict = {}
     for p in programs:
-        prog_off.append(prog_off[-1] + encode_program(p, recs, cache))
+        prog_off.append(prog_off[-1] + encode_program(p, recs, cache, gpu_features))
     lens = np.fromiter((len(r) for r in recs), dtype=np.int64, count=len(recs))
     stmt_off = np.zeros(len(recs) + 1, dtype=np.int64)
     np.cumsum(lens, out=stmt_off[1:])

@@ -15,10 +15,12 @@ from .encode import encode_batch
 N_FEATURES = 164
 
 
-def extract_features_batch(programs) -> list:
-    """One (n_statements x 164) float64 matrix per program, in order."""
+def extract_features_batch(programs, gpu_features: bool = False) -> list:
+    """One (n_statements x 164) float64 matrix per program, in order.
+    gpu_features: fill the 8 gpu_* slots (columns 51-58) with the statement's
+    kernel binding instead of the reference's zeros (opt-in)."""
     lib = rt.load()
-    words, stmt_off, prog_off = encode_batch(programs)
+    words, stmt_off, prog_off = encode_batch(programs, gpu_features)
     n_stmt = len(stmt_off) - 1
     rows = np.empty((n_stmt, N_FEATURES), dtype=np.float64)
     if n_stmt:
@@ -27,5 +29,5 @@ def extract_features_batch(programs) -> list:
     return [rows[prog_off[i]:prog_off[i + 1]] for i in range(len(programs))]
 
 
-def extract_features(program) -> np.ndarray:
-    return extract_features_batch([program])[0]
+def extract_features(program, gpu_features: bool = False) -> np.ndarray:
+    return extract_features_batch([program], gpu_features)[0]

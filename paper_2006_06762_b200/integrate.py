@@ -21,6 +21,11 @@ Search semantics are untouched: with identical scores the batched evolve makes
 the same draws and returns the same candidates as the reference's (tested in
 tests/test_integrate.py).
 
+Opt-in (`install(loomtune, gpu_features=True)`): the
+8 `gpu_*` feature slots the reference leaves zero carry each statement's kernel
+binding (blockIdx, threadIdx, vthread, shared bytes) in training rows and in
+population scoring, so the cost model can tell launch shapes apart.
+
 Opt-in (`install(loomtune, gpu_sampler=True)`): fresh
 samples go through `make_gpu_sampler`, which keeps drawing with the reference's
 own `sample_program` until the State has a legal, GPU-sane launch (the
@@ -123,7 +128,7 @@ def make_gpu_sampler(sample_program, tries: int = 64):
     return sample
 
 
-def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True) -> dict:
+def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_features: bool = False) -> dict:
     """Rebind the reference's hot-path call sites; returns the originals.
 
     gpu_train: `train` fits its trees on the GPU (`gbdt.train`, bit-identical
@@ -140,8 +145,20 @@ def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True) -> dict
     def train(records, hyper=None):
         if gpu_train:
             from . import gbdt
-            return gbdt.train(records, hyper)
-        return GpuCostModel.wrap(ref_train(records, hyper) if hyper is not None else ref_train(records))
+            m = gbdt.train(records, hyper)
+        else:
+            m = GpuCostModel.wrap(ref_train(records, hyper) if hyper is not None else ref_train(records))
+        m.gpu_features = gpu_features
+        return m
+
+    orig["attach_features"] = sched.attach_features
+    if gpu_features:            # opt-in: training rows carry the kernel binding
+        from .features import extract_features
+
+        def attach_features(record, program):
+            record.feats = extract_features(program, gpu_features=True)
+            return record
+        sched.attach_features = attach_features
 
     logio = importlib.import_module(loomtune.__name__ + ".logio")
     orig["cli.cmd_replay"] = cli.cmd_replay
@@ -173,6 +190,8 @@ def uninstall(loomtune, orig: dict) -> None:
     sched.evolve = orig["evolve"]
     cli.measure_batch = orig["cli.measure_batch"]
     sched.sample_program = orig["sample_program"]
+    if "attach_features" in orig:
+        sched.attach_features = orig["attach_features"]
     if "cli.cmd_replay" in orig:
         cli.cmd_replay = orig["cli.cmd_replay"]
         importlib.import_module(loomtune.__name__ + ".logio").LogWriter.write = orig["logio.LogWriter.write"]

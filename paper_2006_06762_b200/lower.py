@@ -557,6 +557,58 @@ def _binding(structure: str):
     return block, vthread, thread, stage, inner
 
 
+def gpu_binding(p, stage) -> tuple:
+    """(blockIdx.x, threadIdx.x, vthread, shared bytes) of the kernel that runs
+    `stage`'s root under this lowering, from the State's tile levels alone (no
+    code generation): the values of the 8 `gpu_*` feature slots the reference
+    leaves zero (src/features.py:63-65,395), for the opt-in GPU feature mode."""
+    smap = {x.name: x for x in p.stages}
+    root = stage
+    while root.compute_at is not None:
+        root = smap[root.compute_at[0]]
+    levels = tile_levels(p, root)
+    points = 1
+    for _, e in root.space:
+        points *= e
+    if levels is None:
+        grid = max(1, min((points + NAIVE_THREADS - 1) // NAIVE_THREADS, 148 * 16))
+        return grid, NAIVE_THREADS, 1, 0
+    structure, factors = levels
+    block, vthread, thread, _, _ = _binding(structure)
+    nb = nt = nv = 1
+    for a, _ in root.space:
+        for lv in block:
+            nb *= factors[a][lv[1]]
+        for lv in thread:
+            nt *= factors[a][lv[1]]
+        for lv in vthread:
+            nv *= factors[a][lv[1]]
+    n_s, n_r = structure.count("S"), structure.count("R")
+    span = {}
+    for a, _ in root.space:
+        t = 1
+        for k in range(1, n_s):
+            t *= factors[a][k]
+        span[a] = t
+    for r, _ in root.reduce:
+        t = 1
+        for k in range(1, n_r):
+            t *= factors[r][k]
+        span[r] = t
+    smem = 0
+    seen = set()
+    for rd in (reads(root.expr.body) if root.reduce else []):
+        key = (rd.buffer, tuple((l.terms, l.const) for l in rd.index))
+        if key in seen:
+            continue
+        seen.add(key)
+        words = 1
+        for lin in rd.index:
+            words *= 1 + sum(abs(c) * (span.get(n, 1) - 1) for n, c in lin.terms)
+        smem += words * 4
+    return nb, nt, nv, smem
+
+
 def _tiled_kernel(ctx: _Ctx, s, levels, entry: str) -> tuple:
     structure, factors = levels
     d = ctx.dtype

@@ -48,6 +48,7 @@ class GpuCostModel:
     hyper: object = field(default_factory=Hyper)
     train_losses: list = field(default_factory=list)
     _handle: int = field(default=0, repr=False, compare=False)
+    gpu_features: bool = field(default=False, compare=False)   # opt-in gpu_* feature slots
 
     # -- construction ------------------------------------------------------
     @staticmethod
@@ -152,7 +153,7 @@ class GpuCostModel:
     def predict_batch(self, programs, return_rows: bool = False):
         """Scores (and optionally the feature rows) of a whole population."""
         lib = rt.load()
-        words, stmt_off, prog_off = encode_batch(programs)
+        words, stmt_off, prog_off = encode_batch(programs, self.gpu_features)
         n_stmt = len(stmt_off) - 1
         scores = np.empty(len(programs), np.float64)
         rows = np.empty((n_stmt, N_FEATURES), np.float64) if return_rows else None

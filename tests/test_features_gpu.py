@@ -97,3 +97,22 @@ def test_column_major_features_and_predict_match_row_major(corpus):
     rt.check(lib.lt_predict_cols_device(m.handle(), cols.data_ptr(), n, b.data_ptr(), sp), "cols")
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+def test_opt_in_gpu_feature_slots(corpus):
+    """gpu_features=True fills columns 51-58 with log2(1 + kernel binding) and
+    leaves every other column exactly as the reference's layout."""
+    from paper_2006_06762_b200.features import extract_features_batch
+    from paper_2006_06762_b200.lower import gpu_binding
+    progs = corpus.programs[:64]
+    base = extract_features_batch(progs)
+    gpu = extract_features_batch(progs, gpu_features=True)
+    for p, a, b in zip(progs, base, gpu):
+        keep = [k for k in range(164) if not 51 <= k <= 58]
+        assert np.array_equal(a[:, keep], b[:, keep])
+        assert not a[:, 51:59].any()
+        live = [s for s in p.stages if not s.inlined]
+        for row, s in zip(b, live):
+            nb, nt, nv, smem = gpu_binding(p, s)
+            want = np.log2(1.0 + np.asarray([nb, 1, 1, nt, 1, 1, nv, smem], np.float64))
+            assert np.allclose(row[51:59], want, rtol=0, atol=1e-12)

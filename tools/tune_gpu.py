@@ -1,6 +1,6 @@
 """Run the reference's unchanged tuner with the B200 hot path installed.
 
-  python tools/tune_gpu.py CFG BUDGET [SEED]
+  python tools/tune_gpu.py CFG BUDGET [SEED] [--gpu-sampler] [--gpu-features]
 
 Imports `loomtune` from baseline/_ref (pip-installed copy of the reference;
 falls back to /root/reference when present), installs the drop-ins
@@ -37,11 +37,12 @@ def main() -> None:
     cfg, budget = sys.argv[1], int(sys.argv[2])
     seed = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 0
     gpu_sampler = "--gpu-sampler" in sys.argv
+    gpu_features = "--gpu-features" in sys.argv
     name, kw = W.CONFIGS[cfg]
     dag = LT.ComputeDAG.from_json(W.build(name, **kw).to_json())
     runner = measure.configure(device=0, cache_dir="")
     sched = importlib.import_module("loomtune.sched")
-    orig = integrate.install(LT, gpu_sampler=gpu_sampler)
+    orig = integrate.install(LT, gpu_sampler=gpu_sampler, gpu_features=gpu_features)
     timers = {"evolve": 0.0, "measure": 0.0, "train": 0.0}
 
     def timed(key, fn):
@@ -68,7 +69,8 @@ def main() -> None:
     wall = time.perf_counter() - t0
     integrate.uninstall(LT, orig)
     best = task.best_cost
-    out = {"config": cfg, "budget": budget, "seed": seed, "gpu_sampler": gpu_sampler, "wall_s": wall, "timers": timers,
+    out = {"config": cfg, "budget": budget, "seed": seed, "gpu_sampler": gpu_sampler, "gpu_features": gpu_features,
+           "wall_s": wall, "timers": timers,
            "measured": len(measured), "valid": sum(m["status"] == "valid" for m in measured),
            "best_us": best, "best_tflops": FLOPS[cfg] / (best * 1e-6) / 1e12,
            "latency_curve": task.latency, "runner": runner.stats,

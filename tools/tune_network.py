@@ -54,7 +54,8 @@ def main() -> None:
                                workers=max(1, (os.cpu_count() or 2) // world - (1 if world == 1 else 0)),
                                lower_workers=max(1, min(8, (os.cpu_count() or 2) // (2 * world))))
     sched = importlib.import_module("loomtune.sched")
-    orig = integrate.install(LT, gpu_sampler=bool(opt.get("--gpu-sampler")))
+    orig = integrate.install(LT, gpu_sampler=bool(opt.get("--gpu-sampler")),
+                             gpu_features=bool(opt.get("--gpu-features")))
     if world > 1:
         from paper_2006_06762_b200 import dist as D
         sched.measure_batch = D.measure_batch_sharded
