@@ -29,6 +29,9 @@ int lt_version(void);
 int lt_device_count(void);
 int lt_set_device(int device);
 void lt_release_scratch(void);
+/* Recover from a kernel fault (sticky error): cudaDeviceReset on `device`; every
+ * task, module, model and training handle created before becomes invalid. */
+int lt_device_reset(int device);
 
 /* ---- (B) feature extraction --------------------------------------------
  * Replaces extract_features / analyze_program / statement_features
@@ -123,6 +126,7 @@ int64_t lt_module_function(int64_t module, const char* name);
 int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads, int* static_smem);
 int64_t lt_task_create(int device);
 void lt_task_destroy(int64_t task);
+void lt_task_abandon(int64_t task);      /* host record only, after lt_device_reset */
 void* lt_task_stream(int64_t task);
 int lt_task_slot(int64_t task, int slot, int64_t bytes);
 int64_t lt_task_slot_ptr(int64_t task, int slot);

@@ -19,6 +19,7 @@ extern "C" int lt_segment_sum_device(const double*, const int64_t*, int64_t, dou
 
 namespace lt {
 
+int g_device_epoch = 0;
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(const std::string& msg) { g_err = msg; return -1; }
@@ -29,6 +30,13 @@ struct Scratch {
   int init() {
     if (!stream && check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream")) return -1;
     return 0;
+  }
+  void forget() {             // after cudaDeviceReset: the pointers are gone, do not free
+    for (DevBuf* b : {&words, &stmt_off, &rows, &cols, &row_scores, &prog_off, &scores, &err}) {
+      b->ptr = nullptr;
+      b->cap = 0;
+    }
+    stream = nullptr;
   }
   void release() {
     for (DevBuf* b : {&words, &stmt_off, &rows, &cols, &row_scores, &prog_off, &scores, &err}) {
@@ -143,6 +151,20 @@ int lt_score_batch(int64_t model, const int32_t* words, const int64_t* stmt_off,
     cudaMemcpyAsync(out_rows, s.rows.ptr, (size_t)n_stmt * 164 * 8, cudaMemcpyDeviceToHost, s.stream);
   }
   return lt::check_cuda(cudaStreamSynchronize(s.stream), "score copy-back");
+}
+
+// Recover from a faulted (sticky-error) context: reset the device and forget
+// every device pointer and per-function attribute this library cached.  Task,
+// module, model and training handles created before become invalid.
+int lt_device_reset(int device) {
+  std::lock_guard<std::mutex> g(lt::g_mu);
+  cudaSetDevice(device);
+  cudaError_t e = cudaDeviceReset();
+  lt::g_s.forget();
+  lt::runner_forget();
+  ++lt::g_device_epoch;
+  cudaGetLastError();
+  return lt::check_cuda(e, "cudaDeviceReset");
 }
 
 void lt_release_scratch(void) {

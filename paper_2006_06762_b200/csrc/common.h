@@ -17,6 +17,10 @@ inline int check_cuda(cudaError_t e, const char* what) {
 }
 inline int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
 
+// incremented by lt_device_reset(): per-function attributes set once per epoch
+extern int g_device_epoch;
+void runner_forget();       // drop cached per-function state (runner.cu)
+
 // Feature columns kept raw (reference src/features.py:74-78): position one-hots of the
 // vectorize/unroll/parallel blocks (cols 19-26, 30-37, 41-48) and, per buffer block b
 // starting at 69+18b, the access one-hot (+0..2) and reuse one-hot (+7..9).

@@ -170,6 +170,11 @@ static int predict_device(int64_t handle, const double* d_rows, int64_t n_rows, 
   if (n_rows <= 0) return 0;
   size_t smem = (size_t)lt::ROWS_PER_BLOCK * (m->n_used + 1) * sizeof(double);
   static size_t configured = 0;
+  static int epoch = -1;
+  if (epoch != lt::g_device_epoch) {
+    configured = 0;
+    epoch = lt::g_device_epoch;
+  }
   if (smem > 48 * 1024 && smem > configured) {
     if (lt::check_cuda(cudaFuncSetAttribute(lt::predict_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "smem attr"))

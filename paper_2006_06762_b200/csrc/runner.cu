@@ -92,6 +92,11 @@ struct Task {
 static std::mutex g_fn_mu;
 static std::unordered_set<CUfunction> g_smem_set;
 
+void runner_forget() {
+  std::lock_guard<std::mutex> g(g_fn_mu);
+  g_smem_set.clear();
+}
+
 __global__ void relerr_kernel(const float* __restrict__ got, const double* __restrict__ ref, int64_t n,
                               unsigned int* __restrict__ out_bits) {
   float local = 0.0f;
@@ -194,6 +199,9 @@ int64_t lt_task_create(int device) {
   }
   return (int64_t)(intptr_t)t;
 }
+
+// Free the host-side task record only (its device objects died with a reset).
+void lt_task_abandon(int64_t handle) { delete (Task*)(intptr_t)handle; }
 
 void lt_task_destroy(int64_t handle) {
   Task* t = (Task*)(intptr_t)handle;

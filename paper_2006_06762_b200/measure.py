@@ -293,6 +293,7 @@ class Runner:
         self._dag_keys: dict = {}          # (id(dag), seed) -> (dag, content key)
         self.modules: OrderedDict = OrderedDict()   # source hash -> (module, funcs)
         self.pinned: set = set()                      # ground-truth modules (held by DAG contexts)
+        self.images: OrderedDict = OrderedDict()      # module key -> cubin (reload after a reset)
         self.mod_lock = threading.Lock()
         self.failed_keys: dict = {}
         self._drain_error = None
@@ -315,6 +316,19 @@ class Runner:
             from concurrent.futures import ProcessPoolExecutor
             self._lpool = ProcessPoolExecutor(self.lower_workers, mp_context=mp.get_context("spawn"))
         return self._lpool
+
+    def reset_device(self) -> None:
+        """After a kernel fault (the context is unusable): reset the device, drop
+        every module and DAG context (re-created on demand) and carry on."""
+        rt.device_reset(self.device)
+        with self.mod_lock:
+            self.modules.clear()
+            self.pinned.clear()
+        for c in self.ctx.values():
+            self.lib.lt_task_abandon(c.task)
+        self.ctx.clear()
+        self._dag_keys.clear()
+        self.stats["device_resets"] = self.stats.get("device_resets", 0) + 1
 
     def forget_compiled(self, cache_dir: str) -> None:
         """Drop every compiled module and restart the compile pool on `cache_dir`
@@ -379,6 +393,12 @@ class Runner:
             if key in self.modules:
                 self.modules.move_to_end(key)
                 return self.modules[key][1]
+            if image:
+                self.images[key] = image        # kept to reload after a device reset
+                while len(self.images) > 1024:
+                    self.images.pop(next(iter(self.images)))
+            else:
+                image = self.images.get(key, b"")
         m = self.lib.lt_module_load(self.device, image, len(image))
         self.io["h2d"] += len(image)
         if not m:
@@ -559,7 +579,16 @@ class Runner:
             print(f"[lt trace] measuring #{i} {key[:12]} {[k.info.get('template') for k in lo.kernels]}",
                   file=sys.stderr, flush=True)
         t0 = time.perf_counter()
-        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        try:
+            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        except rt.NativeError as e:
+            if "kernel fault" not in str(e):
+                raise
+            # a faulting candidate is INVALID like any other failure (SPEC.md:522:
+            # measure_batch never raises); the device is reset and the batch continues
+            rec.detail = "gpu: " + str(e).split(": ", 1)[-1][:200]
+            self.reset_device()
+            return
         self.stats["gpu_s"] += time.perf_counter() - t0
         self.stats["measured"] += 1
         self.io["d2h"] += 4                                 # the max-relative-error word
@@ -595,7 +624,13 @@ class Runner:
             return None
         funcs = self.load(key + (":O1" if opts == PTX_SAFE_OPTS else ":O3"), data, entries)
         t0 = time.perf_counter()
-        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        try:
+            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        except rt.NativeError as e:
+            if "kernel fault" not in str(e):
+                raise
+            self.reset_device()
+            return None
         self.stats["gpu_s"] += time.perf_counter() - t0
         self.io["d2h"] += 4
         return m

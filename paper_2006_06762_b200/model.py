@@ -49,6 +49,7 @@ class GpuCostModel:
     train_losses: list = field(default_factory=list)
     _handle: int = field(default=0, repr=False, compare=False)
     gpu_features: bool = field(default=False, compare=False)   # opt-in gpu_* feature slots
+    _epoch: int = field(default=-1, repr=False, compare=False)
 
     # -- construction ------------------------------------------------------
     @staticmethod
@@ -92,8 +93,9 @@ class GpuCostModel:
 
     # -- device model --------------------------------------------------------
     def handle(self) -> int:
-        if self._handle:
+        if self._handle and self._epoch == rt.epoch:
             return self._handle
+        self._handle = 0                    # created before a device reset: gone
         lib = rt.load()
         n = len(self.trees)
         off = np.zeros(n + 1, np.int64)
@@ -109,11 +111,11 @@ class GpuCostModel:
                                 rt.ptr(eta, rt.c_f64p), float(self.base), N_FEATURES)
         if not h:
             raise rt.NativeError(f"lt_model_create: {lib.lt_last_error().decode()}")
-        self._handle = h
+        self._handle, self._epoch = h, rt.epoch
         return h
 
     def __del__(self):
-        if self._handle and rt._lib is not None:
+        if self._handle and self._epoch == rt.epoch and rt._lib is not None:
             try:
                 rt._lib.lt_model_destroy(self._handle)
             except Exception:

@@ -14,6 +14,7 @@ import numpy as np
 from . import build as _build
 
 _lib = None
+epoch = 0       # incremented by device_reset(); handles from an older epoch are dead
 
 c_i32p = ctypes.POINTER(ctypes.c_int32)
 c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -51,6 +52,8 @@ _SIGS = [
     ("lt_score_batch", ctypes.c_int, [ctypes.c_int64, c_i32p, c_i64p, ctypes.c_int64, c_i64p, ctypes.c_int64,
                                       c_f64p, c_f64p]),
     ("lt_release_scratch", None, []),
+    ("lt_device_reset", ctypes.c_int, [ctypes.c_int]),
+    ("lt_task_abandon", None, [ctypes.c_int64]),
     # GBDT training (csrc/gbdt.cu)
     ("lt_gbdt_create", ctypes.c_int64, [c_f64p, ctypes.c_int64, ctypes.c_int]),
     ("lt_gbdt_destroy", None, [ctypes.c_int64]),
@@ -126,3 +129,11 @@ def check(rc: int, what: str) -> None:
 
 def ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(ctype)
+
+
+def device_reset(device: int) -> None:
+    """Recover from a kernel fault: reset the device (lt_device_reset) and bump
+    the epoch so device-side handles (models, scratch) are re-created."""
+    global epoch
+    check(load().lt_device_reset(device), "device reset")
+    epoch += 1

@@ -124,3 +124,25 @@ def test_baseline_configs_measure(corpus, runner):
     for k, r in enumerate(recs):
         if r.status == VALID:
             print("  ", corpus.entries[idx[k]]["dag"], f"{r.cost_us:.1f} us", r.info["kernels"][0].get("template"))
+
+
+def test_device_reset_recovery():
+    """After a kernel fault the runner resets the device (lt_device_reset) and
+    carries on: modules reload from kept cubins, DAG contexts and the cost
+    model's device handle are re-created."""
+    import numpy as np
+    from paper_2006_06762_b200 import measure
+    from paper_2006_06762_b200.model import GpuCostModel
+    from paper_2006_06762_b200.state import build, naive_program
+    r = measure.configure(device=0, cache_dir="")
+    dag = build("matmul", n=64, m=64, k=64)
+    p = naive_program(dag)
+    (a,) = r.measure_programs([p])
+    m = GpuCostModel(base=1.0)
+    s0 = m.predict_batch([p])
+    r.reset_device()
+    assert r.stats["device_resets"] == 1
+    (b,) = r.measure_programs([p])          # same kernel: reloaded from the kept cubin
+    assert a.status == b.status == "valid"
+    assert np.array_equal(m.predict_batch([p]), s0)
+    measure._shutdown()
