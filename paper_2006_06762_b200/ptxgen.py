@@ -1500,7 +1500,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # pushed below that lose more latency hiding than the overlap wins)
     occ1 = _blocks_per_sm(n_threads, n_acc, smem_bytes)
     occ2 = _blocks_per_sm(n_threads, n_acc, 2 * smem_bytes)
-    spill_heavy = acc_in_regs and n_acc + SPILL_MARGIN > min(255, 65536 // n_threads)
+    spill_heavy = acc_in_regs and n_acc + SPILL_MARGIN > min(255, 65536 // n_threads) and "spillasync" not in _OFF
     use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and not spill_heavy and
                  all(o["read"].buffer not in attached_prod for o in operands) and
                  (occ2 >= occ1 or occ2 * -(-n_threads // 32) >= 4))
