@@ -1546,12 +1546,22 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         g("cp.async.wait_group 0;")
         smem_bytes = 2 * buf
     elif not double:
+        # single-buffered: plain operands still move by cp.async (no register
+        # round trip), others through registers
+        copy1 = (not spill_heavy and "async1" not in _OFF and
+                 all(o["read"].buffer not in attached_prod for o in operands))
+
         def stage_rec(i, sd):
             if i == len(stage_axes):
                 sdig = lambda r, sd=sd: sd.get(r, Aff.k(0))  # noqa: E731
                 g.push()
-                items = fetch_load(sdig)
-                fetch_store(items, sm)
+                if copy1:
+                    fetch_async(sdig, sm, None)
+                    g("cp.async.commit_group;")
+                    g("cp.async.wait_group 0;")
+                else:
+                    items = fetch_load(sdig)
+                    fetch_store(items, sm)
                 g.pop()
                 g("bar.sync 0;")
                 compute(sdig, sm)
