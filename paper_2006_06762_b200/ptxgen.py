@@ -522,6 +522,37 @@ class _Kern:
             return self.gload(buf, idx, guard)
         return read
 
+    def zfill_producer(self, name: str) -> bool:
+        """An attached producer of the form Select(cond, Read(buf, affine), 0) — the
+        padding stage — which a zero-filling cp.async can stage directly."""
+        s = self.m.live.get(name)
+        if s is None or s.reduce or kind(s.expr) != "Select":
+            return False
+        e = s.expr
+        return (kind(e.then) == "Read" and kind(e.other) == "Const" and float(e.other.value) == 0.0
+                and not list(reads(e.cond)) and e.then.buffer not in self.m.live
+                and self.m.layouts.get(e.then.buffer) is None)
+
+    def zfill_source(self, name: str, idx: list) -> tuple:
+        """(64-bit address register, byte immediate, predicate) of a zero-fill
+        producer's element: the Read's element when the condition holds, else
+        the buffer base (a valid address that is never read: src-size 0)."""
+        g = self.g
+        s = self.m.live[name]
+        env = {n: a for (n, _), a in zip(s.space, idx)}
+        ex = Expr(g, lambda n: env[n], None)
+        c = ex(s.expr.cond)
+        p = g.new("%p")
+        g(f"setp.ne.{g.ft} {p}, {c}, {g.fconst(0.0)};")
+        rd = s.expr.then
+        base, flat = self.gsource(rd.buffer, [ex.lin(l) for l in rd.index])
+        rb, imm = g.gaddr(base, flat)
+        a = g.new("%rd")
+        g(f"add.s64 {a}, {rb}, {imm};")
+        sel = g.new("%rd")
+        g(f"selp.b64 {sel}, {a}, {base}, {p};")
+        return sel, 0, p
+
     def producer(self, name: str, idx: list, guard) -> str:
         g = self.g
         s = self.m.live[name]
@@ -1231,13 +1262,18 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                         if pnext is not None:
                             g(f"and.pred {pt}, {pt}, {pnext};")
                         cs = g.decompose(er, o["hull"])
-                        gb, flat = k.gsource(r.buffer, [b_ + Aff.reg(c) for b_, c in zip(base, cs)])
-                        rb, imm = g.gaddr(gb, flat)
+                        idx_ = [b_ + Aff.reg(c) for b_, c in zip(base, cs)]
+                        zp = None
+                        if r.buffer in attached_prod:
+                            rb, imm, zp = k.zfill_source(r.buffer, idx_)
+                        else:
+                            gb, flat = k.gsource(r.buffer, idx_)
+                            rb, imm = g.gaddr(gb, flat)
                         saddr = Aff.k(o["base_word"])
                         for c, st_ in zip(cs, o["stride"]):
                             saddr = saddr + Aff.reg(c, st_)
                         emit_cp(g.aff(saddr.runtime()) if saddr.runtime().terms else None, saddr.const, buf, pt,
-                                rb, imm)
+                                rb, imm, zp)
                 k.loop(-(-trips // FETCH_CHUNK), False, chunk)
                 continue
             for t in range(trips):
@@ -1248,6 +1284,10 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     if pnext is not None:
                         pt = g.new("%p")
                         g(f"and.pred {pt}, {tail}, {pnext};")
+                if r.buffer in attached_prod:           # zero-fill producer (padding)
+                    rb, imm, zp = k.zfill_source(r.buffer, [b_ + c for b_, c in zip(base, cs)])
+                    emit_cp(sa, sc, buf, pt, rb, imm, zp)
+                    continue
                 if ptr is None:             # packed layout: element address per stage
                     gb, flat = k.gsource(r.buffer, [b_ + c for b_, c in zip(base, cs)])
                     rb, imm = g.gaddr(gb, flat)
@@ -1270,7 +1310,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     rb = ptr[0]
                 emit_cp(sa, sc, buf, pt, rb, flat.const * g.esz)
 
-    def emit_cp(sa, sc, buf, pt, rb, imm):
+    def emit_cp(sa, sc, buf, pt, rb, imm, zpred=None):
         key = ("sst", sa, buf)
         a = g.cached(key)
         if a is None:
@@ -1281,7 +1321,12 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {buf};")
             g.remember(key, a)
         pred = f"@{pt} " if pt else ""
-        g(f"{pred}cp.async.ca.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], {g.esz};")
+        if zpred is None:
+            g(f"{pred}cp.async.ca.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], {g.esz};")
+        else:                   # zero-fill where the producer's condition fails
+            n = g.new("%r")
+            g(f"selp.u32 {n}, {g.esz}, 0, {zpred};")
+            g(f"{pred}cp.async.ca.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], {g.esz}, {n};")
 
     # address coefficients: shared-memory word address of operand o as
     #   const0 + sum over local level digits (axis, level) of coef * digit
@@ -1501,8 +1546,10 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     occ1 = _blocks_per_sm(n_threads, n_acc, smem_bytes)
     occ2 = _blocks_per_sm(n_threads, n_acc, 2 * smem_bytes)
     spill_heavy = acc_in_regs and n_acc + SPILL_MARGIN > min(255, 65536 // n_threads) and "spillasync" not in _OFF
+    async_ok = all(o["read"].buffer not in attached_prod or
+                   ("zfill" not in _OFF and k.zfill_producer(o["read"].buffer)) for o in operands)
     use_async = (n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and "async" not in _OFF and not spill_heavy and
-                 all(o["read"].buffer not in attached_prod for o in operands) and
+                 async_ok and
                  (occ2 >= occ1 or occ2 * -(-n_threads // 32) >= 4))
     double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
@@ -1548,8 +1595,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     elif not double:
         # single-buffered: plain operands still move by cp.async (no register
         # round trip), others through registers
-        copy1 = (not spill_heavy and "async1" not in _OFF and
-                 all(o["read"].buffer not in attached_prod for o in operands))
+        copy1 = not spill_heavy and "async1" not in _OFF and async_ok
 
         def stage_rec(i, sd):
             if i == len(stage_axes):
