@@ -146,3 +146,26 @@ def test_device_reset_recovery():
     assert a.status == b.status == "valid"
     assert np.array_equal(m.predict_batch([p]), s0)
     measure._shutdown()
+
+
+def test_naive_multi_point_steps_verify():
+    """The naive template's LT_NAIVE_POINTS option (several output points per
+    grid-stride step, guarded loads and stores for the tail) verifies on naive
+    stream candidates, reductions and fused padding included."""
+    from bench import load_stream
+    from paper_2006_06762_b200 import measure, ptxgen
+    from paper_2006_06762_b200.state import replay
+    r = measure.configure(device=0, cache_dir="", lower_workers=1)   # lower in-process
+    old = ptxgen.NAIVE_POINTS
+    ptxgen.NAIVE_POINTS = 4
+    try:
+        for cfg in ("RC", "G10", "CL"):
+            dag, stream = load_stream(cfg)
+            progs = [replay(dag, h) for h in stream[:12]]
+            recs = r.measure_programs(progs)
+            naive = [x for x in recs if any(k.get("points_per_thread_step") == 4 for k in x.info.get("kernels", []))]
+            assert naive, cfg
+            assert all(x.status == "valid" for x in recs), [(x.status, x.detail) for x in recs]
+    finally:
+        ptxgen.NAIVE_POINTS = old
+        measure._shutdown()
