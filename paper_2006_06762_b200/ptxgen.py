@@ -1454,25 +1454,19 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         def region(i, cv):
             """Fully unrolled suffix of the nest: emit operand loads LOOKAHEAD
             statements ahead of their FMAs (software pipelining of the shared loads)."""
-            snaps = []
-
-            def enum(j):
-                if j == len(loop_list):
-                    snaps.append(dict(cv))
-                    return
-                a, lv, ext, _ = loop_list[j]
-                for val in range(ext):
-                    cv[(a, lv)] = val
-                    enum(j + 1)
-                del cv[(a, lv)]
-            enum(i)
-            plan = []
-            for sn in snaps:
-                ai = 0
-                for kv, val in sn.items():
-                    ai += acc_coef.get(kv, 0) * val
-                plan.append((ai, smem_addr(body.lhs.buffer, body.lhs.index, sn),
-                             smem_addr(body.rhs.buffer, body.rhs.index, sn)))
+            # every statement's accumulator index and operand word offsets are the
+            # fixed (outer) digits' part plus a mixed-radix sum over the enumerated
+            # levels (innermost fastest): computed for all statements at once
+            oa, ca = smem_addr(body.lhs.buffer, body.lhs.index, cv)
+            ob, cb = smem_addr(body.rhs.buffer, body.rhs.index, cv)
+            ai0 = sum(acc_coef.get(kv, 0) * val for kv, val in cv.items())
+            ext = [x[2] for x in loop_list[i:]]
+            keys = [(x[0], x[1]) for x in loop_list[i:]]
+            grid = np.indices(ext).reshape(len(ext), -1) if ext else np.zeros((0, 1), np.int64)
+            ais = ai0 + np.asarray([acc_coef.get(kv, 0) for kv in keys], np.int64) @ grid
+            cas = ca + np.asarray([oa["coef"].get(kv, 0) for kv in keys], np.int64) @ grid
+            cbs = cb + np.asarray([ob["coef"].get(kv, 0) for kv in keys], np.int64) @ grid
+            plan = [(int(x), (oa, int(y)), (ob, int(z))) for x, y, z in zip(ais, cas, cbs)]
             nxt = 0
             for si, (ai, la, lb) in enumerate(plan):
                 while nxt < len(plan) and nxt <= si + LOOKAHEAD:
