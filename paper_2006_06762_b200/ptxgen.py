@@ -770,11 +770,12 @@ def _args(k: _Kern, mod: _Mod, s) -> list:
 
 
 def _bank_degree(coord_sets, st) -> int:
-    banks: dict = {}
-    for coords in coord_sets:
-        addr = sum(c * s_ for c, s_ in zip(coords, st))
-        banks.setdefault(addr % 32, set()).add(addr)
-    return max(len(v) for v in banks.values()) if banks else 1
+    """Worst number of distinct words one shared-memory bank serves for the
+    warp's accesses (coordinates: one row per lane)."""
+    if coord_sets is None or len(coord_sets) == 0:
+        return 1
+    addr = np.unique(np.asarray(coord_sets, np.int64) @ np.asarray(st, np.int64))
+    return int(np.bincount(addr % 32, minlength=32).max())
 
 
 def _smem_strides(hull: list, lane_coords, order=None, step: int = 1, store_coords=None) -> tuple:
