@@ -654,6 +654,22 @@ class _Kern:
 NAIVE_POINTS = int(os.environ.get("LT_NAIVE_POINTS", "1"))
 
 
+def _dec(g: Ptx, d, lv: dict) -> Aff:
+    """A decode AST (src/ir.py:73-93) over loop values `lv` as an Aff."""
+    kk = kind(d)
+    if kk == "DVar":
+        return lv[d.loop]
+    if kk == "DConst":
+        return Aff.k(d.value)
+    if kk == "DAdd":
+        return _dec(g, d.a, lv) + _dec(g, d.b, lv)
+    a = _dec(g, d.a, lv)
+    if kk == "DMul":
+        return a.scale(d.c)
+    r = g.aff(a)
+    return Aff.reg(g.udiv(r, d.c) if kk == "DDiv" else g.urem(r, d.c))
+
+
 def _naive(mod: _Mod, s, entry: str) -> tuple:
     """One output point per thread-iteration (the State's own loops and decode
     maps, reductions serial), NAIVE_POINTS points per grid-stride step so each
@@ -684,18 +700,7 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
     g.push()
 
     def dec(d, lv):
-        kk = kind(d)
-        if kk == "DVar":
-            return lv[d.loop]
-        if kk == "DConst":
-            return Aff.k(d.value)
-        if kk == "DAdd":
-            return dec(d.a, lv) + dec(d.b, lv)
-        a = dec(d.a, lv)
-        if kk == "DMul":
-            return a.scale(d.c)
-        r = g.aff(a)
-        return Aff.reg(g.udiv(r, d.c) if kk == "DDiv" else g.urem(r, d.c))
+        return _dec(g, d, lv)
 
     # per point u: index, guard (u = 0 is in range inside the loop), decoded space env
     pts = []
@@ -763,6 +768,201 @@ def _naive(mod: _Mod, s, entry: str) -> tuple:
     args = _args(k, mod, s)
     return k, Kernel(entry, grid, NAIVE_THREADS, 0, args, {"template": "naive", "stage": s.name, "points": total,
                                                             "points_per_thread_step": U})
+
+
+XREDUCE_MAX_THREADS = 1024
+
+
+def _xreduce_pairs(mod: _Mod) -> dict:
+    """{partial stage: final stage} for every rule-6 pair (ReductionFactorization,
+    `src/sketch.py:307-329`; `_apply_rfactor` `src/ir.py:667-722`) that lowers as
+    ONE cross-thread reduction kernel: the final stage reduces `X.rf` over `rf`
+    exactly as `_apply_rfactor` builds it, the partial is read by nothing else,
+    neither stage is attached, and the partial's space loops enumerate
+    (rf, space...) in row-major order (checked on sample points, so a State
+    whose loops were reordered keeps the two-kernel naive lowering)."""
+    from .state.expr import Lin
+    from .state.ir import d_eval, d_vars
+    if "xreduce" in _OFF:
+        return {}
+    p, out = mod.p, {}
+    for F in p.stages:
+        P = mod.live.get(F.name + ".rf")
+        if F.inlined or F.compute_at is not None or P is None or P.compute_at is not None:
+            continue
+        e, pe = F.expr, P.expr
+        if kind(e) != "Reduce" or kind(pe) != "Reduce" or e.op not in ("sum", "max") or pe.op != e.op:
+            continue
+        if not P.space or len(F.reduce) != 1 or F.reduce[0] != P.space[0] or tuple(P.space[1:]) != tuple(F.space):
+            continue
+        rf = P.space[0][0]
+        want = (Lin.var(rf),) + tuple(Lin.var(n) for n, _ in F.space)
+        if kind(e.body) != "Read" or e.body.buffer != P.name or tuple(e.body.index) != want:
+            continue
+        if P.name in p.dag.outputs or any(st.name != F.name and mod.reads(st.expr, P.name)
+                                          for st in mod.live.values()):
+            continue
+        if any(not mod.reads(P.expr, c.name) for c in mod.attached(P.name)):
+            continue
+        if any(not mod.reads(c.expr, F.name) for c in mod.attached(F.name)):
+            continue
+        sp = [l for l in P.loops if l.kind == "space"]
+        ext = [l.extent for l in sp]
+        total = int(np.prod(ext)) if ext else 1
+        names = [n for n, _ in P.space]
+        dims = [x for _, x in P.space]
+        dmap = dict(P.index_map)
+        sp_ids = {l.id for l in sp}
+        if total != int(np.prod(dims)) or any(n not in dmap or not d_vars(dmap[n]) <= sp_ids for n in names):
+            continue
+        rng = np.random.default_rng(0)
+        qs = set(range(min(total, 64))) | set(range(max(0, total - 64), total))
+        qs |= set(int(x) for x in rng.integers(0, total, 128))
+        ok = True
+        for q in sorted(qs):
+            env, r = {}, q
+            for l in reversed(sp):
+                env[l.id] = r % l.extent
+                r //= l.extent
+            r = q
+            for n, x in zip(reversed(names), reversed(dims)):
+                if d_eval(dmap[n], env) != r % x:
+                    ok = False
+                    break
+                r //= x
+            if not ok:
+                break
+        if ok:
+            out[P.name] = F
+    return out
+
+
+def _xreduce(mod: _Mod, P, F, entry: str) -> tuple:
+    """A rule-6 pair as one cross-thread reduction (the GPU lowering of rfactor:
+    rf -> threadIdx.x).  One block per output point of the final stage
+    (grid-stride), thread t owns rf = t, t+T, ... and runs the partial stage's
+    own reduction loops serially over rk; the block then combines the partials
+    with warp shuffles and one shared-memory round, and thread 0 writes the point
+    (with the final stage's fused consumers).  The partial buffer never exists."""
+    f = P.space[0][1]
+    S = 1
+    for _, x in F.space:
+        S *= x
+    if f * S >= (1 << 31):
+        raise Unsupported("index space exceeds 2^31")
+    T = min(XREDUCE_MAX_THREADS, -(-f // 32) * 32)
+    n_it = -(-f // T)
+    grid = max(1, min(S, 148 * 16))
+    k = _Kern(mod, entry, T)
+    g = k.g
+    op = F.expr.op
+    mv = "b32" if g.ft == "f32" else "b64"
+    ident = g.fconst(0.0 if op == "sum" else -math.inf)
+    comb = "add.rn" if op == "sum" else "max"
+    sp_loops = [l for l in P.loops if l.kind == "space"]
+    rd_loops = [l for l in P.loops if l.kind != "space"]
+    dmap = dict(P.index_map)
+    pnames = [n for n, _ in P.space]
+    body = P.expr.body
+    flags = _unroll_flags([l.extent for l in rd_loops], P.pragma_unroll)
+    tid, sidx = g.new("%r"), g.new("%r")
+    g(f"mov.u32 {tid}, %tid.x;")
+    g(f"mov.u32 {sidx}, %ctaid.x;")
+    n_warp = T // 32
+    if n_warp > 1:
+        lane, warp, sm = g.new("%r"), g.new("%r"), g.new("%r")
+        g(f"and.b32 {lane}, {tid}, 31;")
+        g(f"shr.u32 {warp}, {tid}, 5;")
+        g(f"mov.u32 {sm}, smem_;")
+        wa, ra = g.new("%r"), g.new("%r")
+        g(f"mad.lo.s32 {wa}, {warp}, {g.esz}, {sm};")
+        g(f"mad.lo.s32 {ra}, {tid}, {g.esz}, {sm};")
+        pl0, pin = g.new("%p"), g.new("%p")
+        g(f"setp.eq.s32 {pl0}, {lane}, 0;")
+        g(f"setp.lt.s32 {pin}, {tid}, {n_warp};")
+    p0 = g.new("%p")
+    g(f"setp.eq.s32 {p0}, {tid}, 0;")
+    top = g.new_label()
+    g.label(top)
+    g.push()
+    acc = g.new(g.fr)
+    g(f"mov.{mv} {acc}, {ident};")
+
+    def one_rf(r: Aff) -> None:
+        guard = None
+        if f % T:
+            rr = g.aff(r)
+            guard = g.new("%p")
+            g(f"setp.lt.s32 {guard}, {rr}, {f};")
+        q = g.aff(r.scale(S) + Aff.reg(sidx))
+        digits = g.decompose(q, [l.extent for l in sp_loops]) if sp_loops else []
+        lv = {l.id: Aff.reg(d) for l, d in zip(sp_loops, digits)}
+        env = {n: _dec(g, dmap[n], lv) for n in pnames}
+        pacc = g.new(g.fr)
+        g(f"mov.{mv} {pacc}, {ident};")
+
+        def rec(i, rlv):
+            if i == len(rd_loops):
+                env2 = dict(env)
+                for n, d in P.index_map:
+                    if n not in pnames:
+                        env2[n] = _dec(g, d, {**lv, **rlv})
+                ex = Expr(g, lambda n: env2[n], k.reader(P, lambda n: env2[n]))
+                ex.guard = guard
+                if op == "sum" and kind(body) == "Bin" and body.op == "mul":
+                    a_, b_ = ex(body.lhs), ex(body.rhs)
+                    g(f"fma.rn.{g.ft} {pacc}, {a_}, {b_}, {pacc};")
+                else:
+                    g(f"{comb}.{g.ft} {pacc}, {pacc}, {ex(body)};")
+                return
+            l = rd_loops[i]
+            k.loop(l.extent, flags[i], lambda v: rec(i + 1, {**rlv, l.id: v}))
+        rec(0, {})
+        if guard is not None:
+            g(f"selp.{mv} {pacc}, {pacc}, {ident}, {guard};")
+        g(f"{comb}.{g.ft} {acc}, {acc}, {pacc};")
+
+    if n_it == 1:
+        one_rf(Aff.reg(tid))
+    else:
+        k.loop(n_it, False, lambda i: one_rf(Aff.reg(tid) + i.scale(T)))
+
+    def warp_reduce(v: str) -> None:
+        for off in (16, 8, 4, 2, 1):
+            t = g.new(g.fr)
+            if g.ft == "f32":
+                g(f"shfl.sync.bfly.b32 {t}, {v}, {off}, 31, -1;")
+            else:
+                lo, hi, lo2, hi2 = (g.new("%r") for _ in range(4))
+                g(f"mov.b64 {{{lo}, {hi}}}, {v};")
+                g(f"shfl.sync.bfly.b32 {lo2}, {lo}, {off}, 31, -1;")
+                g(f"shfl.sync.bfly.b32 {hi2}, {hi}, {off}, 31, -1;")
+                g(f"mov.b64 {t}, {{{lo2}, {hi2}}};")
+            g(f"{comb}.{g.ft} {v}, {v}, {t};")
+
+    warp_reduce(acc)
+    if n_warp > 1:
+        g(f"@{pl0} st.shared.{g.ft} [{wa}], {acc};")
+        g("bar.sync 0;")
+        g(f"mov.{mv} {acc}, {ident};")
+        g(f"@{pin} ld.shared.{g.ft} {acc}, [{ra}];")
+        warp_reduce(acc)
+    k.store_guard = p0
+    fdig = g.decompose(sidx, [x for _, x in F.space]) if F.space else []
+    k.epilogue(F, {n: Aff.reg(d) for (n, _), d in zip(F.space, fdig)}, acc, mod.must_materialize(F))
+    k.store_guard = None
+    g.pop()
+    if grid < S:
+        if n_warp > 1:
+            g("bar.sync 0;")                    # the next point reuses the shared slots
+        pe = g.new("%p")
+        g(f"add.s32 {sidx}, {sidx}, {grid};")
+        g(f"setp.lt.s32 {pe}, {sidx}, {S};")
+        g(f"@{pe} bra {top};")
+    smem = n_warp * g.esz if n_warp > 1 else 0
+    return k, Kernel(entry, grid, T, smem, _args(k, mod, F),
+                     {"template": "xreduce", "stage": F.name, "partial": P.name, "points": S, "rf": f,
+                      "threads": T, "rf_per_thread": n_it})
 
 
 def _args(k: _Kern, mod: _Mod, s) -> list:
@@ -1731,15 +1931,19 @@ def lower_ptx(p, dtype: str = "float") -> Lowered:
         raise LoweringError("program has unresolved symbolic extents")
     mod = _Mod(p, dtype)
     kernels, texts = [], []
+    pairs = _xreduce_pairs(mod)
+    fused = {F.name for F in pairs.values()}
     for s in p.stages:
-        if s.inlined or s.compute_at is not None:
+        if s.inlined or s.compute_at is not None or s.name in fused:
             continue
         for c in _attached(p, s.name):
             if _attached(p, c.name) and any(_reads_buffer(c.expr, gg.name) for gg in _attached(p, c.name)):
                 raise LoweringError(f"nested producer attachment under {c.name} is not supported")
         entry = f"k{len(kernels)}_" + ident(s.name)
-        levels = tile_levels(p, s)
-        if levels is not None:
+        levels = tile_levels(p, s) if s.name not in pairs else None
+        if s.name in pairs:
+            kk, kern = _xreduce(mod, s, pairs[s.name], entry)
+        elif levels is not None:
             kk, kern = _tiled(mod, s, levels, entry)
         else:
             kk, kern = _naive(mod, s, entry)
@@ -1747,7 +1951,7 @@ def lower_ptx(p, dtype: str = "float") -> Lowered:
         kernels.append(kern)
         texts.append(kk.text())
     for name, st in mod.live.items():
-        if name not in mod.buffers:
+        if name not in mod.buffers and name not in pairs:      # a fused partial never exists
             mod.buffers[name] = Buffer(name, tuple(e for _, e in st.space),
                                        "output" if name in p.dag.outputs else "temp")
     head = ".version 8.7\n.target sm_100a\n.address_size 64\n.extern .shared .align 16 .b8 smem_[];\n"
