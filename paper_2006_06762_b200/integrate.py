@@ -31,6 +31,11 @@ samples go through `make_gpu_sampler`, which keeps drawing with the reference's
 own `sample_program` until the State has a legal, GPU-sane launch (the
 reference's CPU-oriented sampler yields ~2% of those for tiled sketches).  This
 changes the search distribution and is off by default.
+
+Opt-in (`gpu_sketch_policy(loomtune, task)`): a task keeps
+only the sketches derived through a GPU rule (multi-level tiling — every tiled
+kernel stages its operands through shared memory, the cache-read rule — or
+reduction factorization, lowered as a cross-thread reduction).
 """
 
 from __future__ import annotations
@@ -126,6 +131,33 @@ def make_gpu_sampler(sample_program, tries: int = 64):
                 return p
         return p
     return sample
+
+
+# rule ids of the reference's sketch rules that give a stage a GPU kernel shape
+# (src/sketch.py:260-329): multi-level tiling, tiling with fusion, reduction
+# factorization (lowered as a cross-thread reduction, ptxgen._xreduce)
+GPU_SKETCH_RULES = frozenset((3, 4, 6))
+
+
+def gpu_sketch_policy(loomtune, task, structure: str = "SSSRRSRS") -> list:
+    """Opt-in GPU sketch policy: Ansor's GPU sketches
+    always tile a data-reuse stage (multi-level tiling staged through shared
+    memory) or bind a factored reduction to threads; the reference's CPU rule
+    table also keeps the untiled derivations (rule 1 `skip` on every node).
+    Keeps, in place and in order, the task's sketches whose rule path uses a GPU
+    rule, when there is one; returns the kept rule paths.  Changes the search
+    space, so it is off by default."""
+    import importlib
+    sk = importlib.import_module(loomtune.__name__ + ".sketch")
+    traced = sk.generate_sketches_traced(task.dag, structure=structure)
+    if len(traced) != len(task.sketches):
+        raise ValueError(f"task {task.name}: sketch list does not match its rule paths")
+    keep = [i for i, (_, path) in enumerate(traced)
+            if any(isinstance(r, int) and r in GPU_SKETCH_RULES for r in path)]
+    if keep and len(keep) < len(traced):
+        task.sketches[:] = [task.sketches[i] for i in keep]
+        return [traced[i][1] for i in keep]
+    return [path for _, path in traced]
 
 
 def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_features: bool = False) -> dict:

@@ -47,6 +47,22 @@ def test_batched_evolve_matches_reference_evolve():
     assert [ev._state_key(c.program) for c in got] == [ev._state_key(c.program) for c in want]
 
 
+def test_gpu_sketch_policy_keeps_gpu_rule_sketches():
+    from paper_2006_06762_b200.integrate import gpu_sketch_policy
+    t = LT.make_task("mm", LT.build("matmul", n=64, m=64, k=64), structure="SSSRRSRS")
+    before = list(t.sketches)
+    paths = gpu_sketch_policy(LT, t)
+    assert paths and all({3, 4, 6} & set(p) for p in paths)
+    assert 0 < len(t.sketches) < len(before)
+    assert all(any(s is b for b in before) for s in t.sketches)        # a subset, order kept
+    n2 = LT.make_task("n2", LT.build("norm2", n=32, m=64), structure="SSSRRSRS")
+    assert [6 in p for p in gpu_sketch_policy(LT, n2)] == [True]        # rfactor -> cross-thread
+    ew = LT.make_task("ew", LT.build("elemwise_chain", n=256), structure="SSSRRSRS")
+    k = len(ew.sketches)
+    gpu_sketch_policy(LT, ew)
+    assert len(ew.sketches) == k                                        # no GPU rule applies: unchanged
+
+
 def test_install_rebinds_and_restores():
     from paper_2006_06762_b200 import integrate, measure
     import importlib

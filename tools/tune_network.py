@@ -3,7 +3,7 @@ reference's unchanged multi-task `tune` (gradient task scheduler,
 `src/sched.py:276-375`) over every distinct ResNet-50 subgraph, with the B200
 hot path installed.
 
-  python tools/tune_network.py BUDGET [SEED] [--batch N] [--gpu-sampler] [--tasks K]
+  python tools/tune_network.py BUDGET [SEED] [--batch N] [--gpu-sampler] [--gpu-sketches] [--tasks K]
 
 Tasks come from `paper_2006_06762_b200.resnet50.tasks` (23 conv shapes + the
 classifier, weights = instance counts).  Under torchrun each rank measures its
@@ -86,6 +86,8 @@ def main() -> None:
     for name, dag, weight in specs:
         ldag = LT.ComputeDAG.from_json(dag.to_json())
         tasks.append(LT.make_task(name, ldag, weight=float(weight), dnn="resnet50", structure="SSSRRSRS"))
+        if opt.get("--gpu-sketches"):
+            integrate.gpu_sketch_policy(LT, tasks[-1])
     t_setup = time.perf_counter() - t0
     t0 = time.perf_counter()
     LT.tune(tasks, LT.Objective(), budget, LT.TuneSettings(batch_size=16), LT.SchedulerParams(), seed=seed,
@@ -102,7 +104,7 @@ def main() -> None:
         net_us += weight * t.best_cost
     naive_net = sum(w * t.naive_cost for (_, _, w), t in zip(specs, tasks))
     out = {"config": "resnet50 whole network", "batch": batch, "budget": budget, "seed": seed, "n_gpus": world,
-           "tasks": len(tasks), "wall_s": wall, "setup_s": t_setup, "timers": timers, **counts,
+           "tasks": len(tasks), "gpu_sketches": bool(opt.get("--gpu-sketches")), "wall_s": wall, "setup_s": t_setup, "timers": timers, **counts,
            "measured_per_s": counts["measured"] / timers["measure"] if timers["measure"] else None,
            "network_latency_us": net_us, "naive_network_latency_us": naive_net,
            "network_tflops": sum(w * resnet50.flops(d) for _, d, w in specs) / (net_us * 1e-6) / 1e12,
