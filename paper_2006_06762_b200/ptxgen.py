@@ -40,6 +40,7 @@ ASYNC_MAX_TRIPS = 64  # cp.async staging: per-operand trips per thread (carry-fr
 # template switches (all on in production; LT_PTX_OFF=promote,plan,pad turns them off for A/B checks)
 _OFF = set(os.environ.get("LT_PTX_OFF", "").split(","))
 FETCH_CHUNK = 1 if "chunk" in _OFF else 8   # loads in flight per thread in a rolled cooperative fetch
+HOIST_SPILL_UNROLLED = 64   # spilling register tiles: reduction-outer order only up to this unrolled body
 
 
 class Unsupported(Exception):
@@ -1131,6 +1132,21 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # the accumulator tile is indexed only by space-level digits: it stays in
     # registers whenever those loops are unrolled (rolled reduction loops are fine)
     acc_in_regs = all(u for x, u in zip(loop_list, unroll) if x[1][0] == "S")
+    tile_spills = n_acc + SPILL_MARGIN > min(255, 65536 // n_threads)
+    if acc_in_regs and "hoist" not in _OFF and (not tile_spills or unrolled <= HOIST_SPILL_UNROLLED):
+        # register tile in registers: every space loop is unrolled, so the thread's
+        # nest is issued reduction loops first (their relative order kept, hence
+        # every accumulator's summation order is unchanged) and the whole tile
+        # innermost — TVM's virtual-thread injection does the same for vthreads.
+        # Each reduction step then loads its operands once for all accumulators
+        # instead of once per vthread / S3 copy around a rolled reduction loop.
+        # A tile that overflows the register file keeps the State's order unless
+        # its reduction is mostly rolled: sweeping all accumulators every step
+        # multiplies its spill traffic (template_bench A/B, 128 States per config).
+        perm = ([i for i, x in enumerate(loop_list) if x[1][0] == "R"]
+                + [i for i, x in enumerate(loop_list) if x[1][0] != "R"])
+        loop_list = [loop_list[i] for i in perm]
+        unroll = [unroll[i] for i in perm]
 
     # smem layout: pad each operand's innermost dim against the warp's bank pattern
     lanes = min(32, n_threads)
