@@ -44,7 +44,10 @@ def best_candidate(cfg: str, n: int, offset: int = 0) -> None:
         json.dump(out, fh)
     with open(os.path.join(ROOT, "gpurun_out", f"best_{cfg}.src"), "w") as fh:
         fh.write(lo.source)
-    funcs = runner.load(key, b"", [k.entry for k in lo.kernels])
+    funcs = []                  # one module per kernel (measure._modules_of), keyed as the runner keys them
+    for ents, text, opts in measure._modules_of(lo):
+        kkey = __import__("hashlib").sha1((opts or "").encode() + text.encode()).hexdigest()
+        funcs += runner.load(kkey, b"", ents)
     ctx = runner.context(p.dag, 0)
     launches = ctx._launches(lo, funcs)
     torch.cuda.synchronize()
