@@ -63,6 +63,18 @@ def test_gpu_sketch_policy_keeps_gpu_rule_sketches():
     assert len(ew.sketches) == k                                        # no GPU rule applies: unchanged
 
 
+def test_gpu_sampler_draws_legal_gpu_sane_states():
+    from loomtune.ir import validate
+    from paper_2006_06762_b200.integrate import gpu_sane, make_gpu_sampler
+    t = LT.make_task("mm", LT.build("matmul", n=256, m=256, k=128), structure="SSSRRSRS")
+    sample = make_gpu_sampler(LT.sample_program)
+    rng = np.random.default_rng(0)
+    for i in range(24):
+        p = sample(t.sketches[i % len(t.sketches)], LT.AnnotationPolicy(), rng)
+        assert p.is_concrete() and not validate(p)
+        assert gpu_sane(p)
+
+
 def test_install_rebinds_and_restores():
     from paper_2006_06762_b200 import integrate, measure
     import importlib
