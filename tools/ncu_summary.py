@@ -46,7 +46,7 @@ def main() -> None:
     seen = set()
     for r in body:
         name = r[ix["Kernel Name"]].split("(")[0]
-        key = (r[ix["ID"]], r[ix["Metric Name"]])
+        key = (name, r[ix["Metric Name"]])          # first launch of each kernel
         if r[ix["Metric Name"]] in KEEP and key not in seen:
             seen.add(key)
             print(f"{name:14s} {r[ix['Section Name']]:34s} {r[ix['Metric Name']]:34s} "
