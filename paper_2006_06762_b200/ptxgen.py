@@ -1233,6 +1233,13 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             if deg1 < deg / o["vec"] or (deg1 == deg / o["vec"] and w1 < o["words"]):
                 o["stride"], o["words"], o["vec"] = st1, w1, 1
                 o["order"] = list(range(len(o["hull"])))
+        dl = len(o["hull"]) - 1
+        if "fvec" not in _OFF and g.ft == "f32" and dl >= 0 and o["order"][-1] == dl and o["hull"][dl] % 4 == 0:
+            # rows padded to 16 bytes when that costs no compute-side conflicts:
+            # the fetch can then move 16-byte quads (fetch_vec)
+            st4, w4, _ = _smem_strides(o["hull"], coords, o["order"], 4, None)
+            if _bank_degree(coords, st4) <= _bank_degree(coords, o["stride"]) and w4 <= o["words"] + o["words"] // 4:
+                o["stride"], o["words"] = st4, w4
         total_words = -(-total_words // 4) * 4          # 16-byte aligned operand bases
         o["base_word"] = total_words
         total_words += o["words"]
@@ -1306,7 +1313,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         """Per fetch trip t, the constant hull-coordinate shift with
         coords(tid + t*threads) == coords(tid) + shift for every live tid, or
         None when some tid carries across a hull digit."""
-        hull = o["hull"]
+        hull = fhull(o)
         tids = np.arange(n_threads, dtype=np.int64)
 
         def digits(e):
@@ -1320,7 +1327,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
         shifts = []
         for t in range(trips):
             e = tids + t * n_threads
-            live = e < o["size"]
+            live = e < fsize(o)
             if not live.any():
                 return None
             dd = digits(e)[live] - d0[live]
@@ -1328,6 +1335,36 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 return None
             shifts.append([int(x) for x in dd[0][1:]])
         return shifts
+
+    # vectorised fetch: an operand whose innermost (global-contiguous) dim is laid
+    # out unit-stride with 16-byte aligned rows in shared memory and whose global
+    # rows and block/stage offsets are multiples of 4 words moves as 16-byte
+    # cp.async quads (o["fv"] = 4): a quarter of the copies and address math
+    def fhull(o):
+        return o["hull"][:-1] + [o["hull"][-1] // o.get("fv", 1)]
+
+    def fsize(o):
+        return o["size"] // o.get("fv", 1)
+
+    def qcoords(o, cs):
+        w = o.get("fv", 1)
+        return cs if w == 1 else cs[:-1] + [cs[-1].scale(w)]
+
+    def fetch_vec(o) -> int:
+        name = o["read"].buffer
+        d = len(o["hull"]) - 1
+        if "fvec" in _OFF or g.ft != "f32" or name in attached_prod or d < 0:
+            return 1
+        if name not in mod.live and mod.layouts.get(name) is not None:
+            return 1
+        if o["order"][-1] != d or o["stride"][d] != 1 or o["hull"][d] % 4 or o["base_word"] % 4:
+            return 1
+        if any(o["stride"][j] % 4 for j in range(d)) or mod.shape(name)[-1] % 4:
+            return 1
+        last = operand_base(o, lambda n: Aff.reg(f"%stage_{n}"))[d]
+        if last.const % 4 or any(c % 4 for c in last.terms.values()):
+            return 1
+        return 4
 
     # loop-invariant part of the cooperative fetch (coordinates, tail predicates,
     # shared-memory addresses, global pointers without the staging offset),
@@ -1344,12 +1381,12 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     def prep_fetch(long_ok=False):
         zero = lambda r: Aff.k(0)  # noqa: E731
         for oi, o in enumerate(operands):
-            trips = -(-o["size"] // n_threads)
+            trips = -(-fsize(o) // n_threads)
             if not plannable(o, trips, long_ok) or "plan" in _OFF:
                 continue
-            full = o["size"] % n_threads == 0
+            full = fsize(o) % n_threads == 0
             shifts = carry_free_shifts(o, trips)
-            cs0 = g.decompose(tid, o["hull"]) if shifts is not None else None
+            cs0 = g.decompose(tid, fhull(o)) if shifts is not None else None
             base0 = operand_base(o, zero)
             name = o["read"].buffer
             plain = name not in attached_prod and (name in mod.live or mod.layouts.get(name) is None)
@@ -1357,11 +1394,12 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 tail = None
                 if not full and t == trips - 1:
                     tail = g.new("%p")
-                    g(f"setp.lt.s32 {tail}, {tid}, {o['size'] - t * n_threads};")
+                    g(f"setp.lt.s32 {tail}, {tid}, {fsize(o) - t * n_threads};")
                 if shifts is not None:
                     cs = [Aff.reg(c) + sh for c, sh in zip(cs0, shifts[t])]
                 else:
-                    cs = [Aff.reg(c) for c in g.decompose(g.aff(Aff.reg(tid) + t * n_threads), o["hull"])]
+                    cs = [Aff.reg(c) for c in g.decompose(g.aff(Aff.reg(tid) + t * n_threads), fhull(o))]
+                cs = qcoords(o, cs)
                 saddr = Aff.k(o["base_word"])
                 for c, st_ in zip(cs, o["stride"]):
                     saddr = saddr + c.scale(st_)
@@ -1467,7 +1505,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             r = o["read"]
             base = operand_base(o, sdig)
             zero_base = operand_base(o, lambda n: Aff.k(0))
-            trips = -(-o["size"] // n_threads)
+            trips = -(-fsize(o) // n_threads)
+            nb = g.esz * o.get("fv", 1)
             if (oi, 0) not in fetch_plan:
                 # no hoistable addressing: a rolled loop over chunks of trips, every
                 # element's coordinates decomposed in place (copies stay asynchronous)
@@ -1475,11 +1514,11 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     for j in range(FETCH_CHUNK):
                         er = g.aff(Aff.reg(tid) + (tv.scale(FETCH_CHUNK) + j).scale(n_threads))
                         pt = g.new("%p")
-                        g(f"setp.lt.s32 {pt}, {er}, {o['size']};")
+                        g(f"setp.lt.s32 {pt}, {er}, {fsize(o)};")
                         if pnext is not None:
                             g(f"and.pred {pt}, {pt}, {pnext};")
-                        cs = g.decompose(er, o["hull"])
-                        idx_ = [b_ + Aff.reg(c) for b_, c in zip(base, cs)]
+                        cs = qcoords(o, [Aff.reg(c) for c in g.decompose(er, fhull(o))])
+                        idx_ = [b_ + c for b_, c in zip(base, cs)]
                         zp = None
                         if r.buffer in attached_prod:
                             rb, imm, zp = k.zfill_source(r.buffer, idx_)
@@ -1488,9 +1527,9 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                             rb, imm = g.gaddr(gb, flat)
                         saddr = Aff.k(o["base_word"])
                         for c, st_ in zip(cs, o["stride"]):
-                            saddr = saddr + Aff.reg(c, st_)
+                            saddr = saddr + c.scale(st_)
                         emit_cp(g.aff(saddr.runtime()) if saddr.runtime().terms else None, saddr.const, buf, pt,
-                                rb, imm, zp)
+                                rb, imm, zp, nb)
                 k.loop(-(-trips // FETCH_CHUNK), False, chunk)
                 continue
             for t in range(trips):
@@ -1508,7 +1547,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 if ptr is None:             # packed layout: element address per stage
                     gb, flat = k.gsource(r.buffer, [b_ + c for b_, c in zip(base, cs)])
                     rb, imm = g.gaddr(gb, flat)
-                    emit_cp(sa, sc, buf, pt, rb, imm)
+                    emit_cp(sa, sc, buf, pt, rb, imm, None, nb)
                     continue
                 flat = k.gflat(r.buffer, [b_ + c for b_, c in zip(base, cs)])
                 inv = k.gflat(r.buffer, [b_ + c for b_, c in zip(zero_base, cs)])
@@ -1525,9 +1564,9 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                         g.remember(k2, rb)
                 else:
                     rb = ptr[0]
-                emit_cp(sa, sc, buf, pt, rb, flat.const * g.esz)
+                emit_cp(sa, sc, buf, pt, rb, flat.const * g.esz, None, nb)
 
-    def emit_cp(sa, sc, buf, pt, rb, imm, zpred=None):
+    def emit_cp(sa, sc, buf, pt, rb, imm, zpred=None, nbytes=None):
         key = ("sst", sa, buf)
         a = g.cached(key)
         if a is None:
@@ -1538,8 +1577,11 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 g(f"mad.lo.s32 {a}, {sa}, {g.esz}, {buf};")
             g.remember(key, a)
         pred = f"@{pt} " if pt else ""
-        if zpred is None:
-            g(f"{pred}cp.async.ca.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], {g.esz};")
+        nbytes = nbytes or g.esz
+        if zpred is None and nbytes == 16:           # 16-byte quads bypass L1 (.cg)
+            g(f"{pred}cp.async.cg.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], 16;")
+        elif zpred is None:
+            g(f"{pred}cp.async.ca.shared.global [{a}+{sc * g.esz}], [{rb}+{imm}], {nbytes};")
         else:                   # zero-fill where the producer's condition fails
             n = g.new("%r")
             g(f"selp.u32 {n}, {g.esz}, 0, {zpred};")
@@ -1764,6 +1806,10 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                  (occ2 >= occ1 or occ2 * -(-n_threads // 32) >= 4))
     double = (not use_async and n_stage > 1 and 2 * smem_bytes <= MAX_SMEM and all(t <= 16 for t in trips_all)
               and sum(trips_all) <= 48)
+    copy1 = not use_async and not double and not spill_heavy and "async1" not in _OFF and async_ok
+    if use_async or copy1:
+        for o in operands:
+            o["fv"] = fetch_vec(o)
     prep_fetch(long_ok=use_async)
     if use_async:
         buf = total_words * g.esz
@@ -1806,8 +1852,6 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     elif not double:
         # single-buffered: plain operands still move by cp.async (no register
         # round trip), others through registers
-        copy1 = not spill_heavy and "async1" not in _OFF and async_ok
-
         def stage_rec(i, sd):
             if i == len(stage_axes):
                 sdig = lambda r, sd=sd: sd.get(r, Aff.k(0))  # noqa: E731
@@ -1911,7 +1955,7 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
             "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx",
             "double_buffered": double or use_async, "async_copy": use_async, "acc_in_regs": acc_in_regs,
-            "n_stage": n_stage}
+            "n_stage": n_stage, "fetch_vec": [o.get("fv", 1) for o in operands]}
     return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
 
 
