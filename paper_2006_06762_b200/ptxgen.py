@@ -1233,13 +1233,6 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             if deg1 < deg / o["vec"] or (deg1 == deg / o["vec"] and w1 < o["words"]):
                 o["stride"], o["words"], o["vec"] = st1, w1, 1
                 o["order"] = list(range(len(o["hull"])))
-        dl = len(o["hull"]) - 1
-        if "fvec" not in _OFF and g.ft == "f32" and dl >= 0 and o["order"][-1] == dl and o["hull"][dl] % 4 == 0:
-            # rows padded to 16 bytes when that costs no compute-side conflicts:
-            # the fetch can then move 16-byte quads (fetch_vec)
-            st4, w4, _ = _smem_strides(o["hull"], coords, o["order"], 4, None)
-            if _bank_degree(coords, st4) <= _bank_degree(coords, o["stride"]) and w4 <= o["words"] + o["words"] // 4:
-                o["stride"], o["words"] = st4, w4
         total_words = -(-total_words // 4) * 4          # 16-byte aligned operand bases
         o["base_word"] = total_words
         total_words += o["words"]
@@ -1339,7 +1332,10 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # vectorised fetch: an operand whose innermost (global-contiguous) dim is laid
     # out unit-stride with 16-byte aligned rows in shared memory and whose global
     # rows and block/stage offsets are multiples of 4 words moves as 16-byte
-    # cp.async quads (o["fv"] = 4): a quarter of the copies and address math
+    # cp.async quads (o["fv"] = 4): a quarter of the copies and address math.
+    # The layout is not changed to make rows 16-byte aligned: re-padding rows
+    # for it measured slower (template_bench A/B: 7 of 30 such States regressed,
+    # up to 3.7x), quads on already aligned layouts 17% faster (geomean, 36 States)
     def fhull(o):
         return o["hull"][:-1] + [o["hull"][-1] // o.get("fv", 1)]
 
