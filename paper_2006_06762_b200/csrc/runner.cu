@@ -171,6 +171,12 @@ int64_t lt_module_function(int64_t module, const char* name) {
   if (!d) return 0;
   CUfunction f;
   if (lt::check_cu(d->ModuleGetFunction(&f, (CUmodule)(intptr_t)module, name), "cuModuleGetFunction")) return 0;
+  {
+    // a handle value can be reused by a module loaded after another was unloaded
+    // (the runner's LRU evicts modules): its dynamic shared-memory grant is new
+    std::lock_guard<std::mutex> g(lt::g_fn_mu);
+    lt::g_smem_set.erase(f);
+  }
   return (int64_t)(intptr_t)f;
 }
 

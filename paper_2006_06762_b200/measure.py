@@ -302,6 +302,7 @@ class Runner:
                       "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0}
         self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
+        self.max_modules = 512          # loaded candidate modules kept (LRU)
         self.lower_workers = (lower_workers if lower_workers is not None
                               else int(os.environ.get("LT_LOWER_WORKERS", max(1, min(8, (os.cpu_count() or 2) // 2)))))
         self._lpool = None
@@ -411,7 +412,7 @@ class Runner:
             funcs.append(f)
         with self.mod_lock:
             self.modules[key] = (m, funcs)
-            while len(self.modules) > 512:          # LRU, never the ground-truth modules
+            while len(self.modules) > self.max_modules:     # LRU, never the ground-truth modules
                 victim = next((k for k in self.modules if k not in self.pinned), None)
                 if victim is None:
                     break

@@ -1336,11 +1336,19 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     # The layout is not changed to make rows 16-byte aligned: re-padding rows
     # for it measured slower (template_bench A/B: 7 of 30 such States regressed,
     # up to 3.7x), quads on already aligned layouts 17% faster (geomean, 36 States)
-    def fhull(o):
+    def fhull_real(o):
         return o["hull"][:-1] + [o["hull"][-1] // o.get("fv", 1)]
 
+    def fhull(o):
+        """Fetch enumeration hull: the real one, or every dim rounded up to a power
+        of two (o["p2"]) so that with a power-of-two block the per-trip coordinates
+        are carry-free (one base register + immediates) instead of divided out per
+        element; elements outside the real hull are predicated off."""
+        h = fhull_real(o)
+        return [1 << (x - 1).bit_length() for x in h] if o.get("p2") else h
+
     def fsize(o):
-        return o["size"] // o.get("fv", 1)
+        return int(np.prod(fhull(o))) if o.get("p2") else o["size"] // o.get("fv", 1)
 
     def qcoords(o, cs):
         w = o.get("fv", 1)
@@ -1395,6 +1403,23 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                     cs = [Aff.reg(c) + sh for c, sh in zip(cs0, shifts[t])]
                 else:
                     cs = [Aff.reg(c) for c in g.decompose(g.aff(Aff.reg(tid) + t * n_threads), fhull(o))]
+                if o.get("p2"):         # padded enumeration: predicate off coordinates beyond the hull
+                    for c, hr, hp in zip(cs, fhull_real(o), fhull(o)):
+                        if hr == hp:
+                            continue
+                        key = ("p2ok", c.key(), c.const, hr)
+                        pv = g.cached(key)
+                        if pv is None:
+                            cr = g.aff(Aff(dict(c.terms)))
+                            pv = g.new("%p")
+                            g(f"setp.lt.s32 {pv}, {cr}, {hr - c.const};")
+                            g.remember(key, pv)
+                        if tail is None:
+                            tail = pv
+                        else:
+                            t2 = g.new("%p")
+                            g(f"and.pred {t2}, {tail}, {pv};")
+                            tail = t2
                 cs = qcoords(o, cs)
                 saddr = Aff.k(o["base_word"])
                 for c, st_ in zip(cs, o["stride"]):
@@ -1806,6 +1831,18 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
     if use_async or copy1:
         for o in operands:
             o["fv"] = fetch_vec(o)
+            if not use_async or "p2" in _OFF or n_threads & (n_threads - 1):
+                continue
+            # power-of-two fetch enumeration where it turns a per-element divided
+            # (rolled) fetch into a carry-free hoisted one at <= 2x idle slots
+            real = fhull_real(o)
+            t1 = -(-fsize(o) // n_threads)
+            if plannable(o, t1, True) or all(x & (x - 1) == 0 for x in real):
+                continue
+            o["p2"] = True
+            t2 = -(-fsize(o) // n_threads)
+            if fsize(o) > 2 * int(np.prod(real)) or not plannable(o, t2, True):
+                o["p2"] = False
     prep_fetch(long_ok=use_async)
     if use_async:
         buf = total_words * g.esz
@@ -1951,7 +1988,8 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
             "blocks": n_blocks, "vthreads": n_vt, "acc": n_acc, "smem": smem_bytes, "unrolled": unrolled,
             "factors": {a: list(v) for a, v in factors.items()}, "backend": "ptx",
             "double_buffered": double or use_async, "async_copy": use_async, "acc_in_regs": acc_in_regs,
-            "n_stage": n_stage, "fetch_vec": [o.get("fv", 1) for o in operands]}
+            "n_stage": n_stage, "fetch_vec": [o.get("fv", 1) for o in operands],
+            "fetch_pow2": [bool(o.get("p2")) for o in operands]}
     return k, Kernel(entry, n_blocks, n_threads, smem_bytes, list(k.params), info)
 
 
