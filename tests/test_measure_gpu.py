@@ -171,19 +171,20 @@ def test_naive_multi_point_steps_verify():
         measure._shutdown()
 
 
-def test_module_eviction_keeps_shared_memory_grants_valid(runner):
+def test_module_eviction_keeps_shared_memory_grants_valid():
     """Candidate modules are evicted LRU; a function handle value reused by a
     later module must get its own >48 KB dynamic shared-memory grant (stale
     grants made such launches fail with 'invalid argument')."""
     from bench import load_stream
+    from paper_2006_06762_b200 import measure
     from paper_2006_06762_b200.state import replay
     dag, stream = load_stream("TBG")
-    cap = runner.max_modules
+    runner = measure.configure(device=0, cache_dir="")
     runner.max_modules = 4
     try:
         recs = runner.measure_programs([replay(dag, h) for h in stream[:48]])
     finally:
-        runner.max_modules = cap
+        measure._shutdown()
     big = [r for r in recs if any((k.get("smem") or 0) > 48 * 1024 for k in r.info.get("kernels", []))]
     assert big
     for i, r in enumerate(recs):
