@@ -512,8 +512,10 @@ class Runner:
             if job is None:
                 continue
             if isinstance(job, tuple):
+                # the other candidate's compile has landed: loaded, failed, or
+                # loaded and already evicted by the LRU (reloaded from its image)
                 with self.mod_lock:
-                    if not (kkey in self.modules or kkey in self.failed_keys):
+                    if not (kkey in self.modules or kkey in self.failed_keys or kkey in self.images):
                         return False
             elif self.lib.lt_compile_ready(job) == 0:
                 return False
