@@ -42,6 +42,8 @@ def main() -> None:
     for cfg in ("RC", "G10", "CL", "TBG"):
         dag, stream = load_stream(cfg)
         feats += ext([replay(dag, h) for h in stream[:max(sizes) // 4 + 1]])
+    while len(feats) < max(sizes):          # beyond the streams: repeat programs (labels differ)
+        feats += feats[:max(sizes) - len(feats)]
     rng = np.random.default_rng(0)
     ref = None
     for cand in (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src"):
