@@ -29,9 +29,21 @@ int lt_version(void);
 int lt_device_count(void);
 int lt_set_device(int device);
 void lt_release_scratch(void);
-/* Recover from a kernel fault (sticky error): cudaDeviceReset on `device`; every
- * task, module, model and training handle created before becomes invalid. */
-int lt_device_reset(int device);
+/* Setup: checks that n_gpus devices are visible, creates each
+ * device's runner context and starts the compile pool (n_workers <= 0: host
+ * cores - 1) with an on-disk cubin cache in cache_dir (NULL/"": none). */
+int lt_init(int n_gpus, const char* cache_dir, int n_workers);
+/* Teardown before process exit: compile pool stopped (workers reaped), runner
+ * contexts destroyed, scratch freed.  Model/training handles stay valid until
+ * their destroy calls. */
+int lt_shutdown(void);
+/* Candidate kernels run in a private per-device "runner" context, never in the
+ * primary context (torch, NCCL, scoring and training kernels).  After a kernel
+ * fault (lt_measure_record.status == 2) lt_runner_reset destroys that context:
+ * every task and candidate module of `device` created before becomes invalid;
+ * nothing else is touched.  lt_runner_generation counts the resets. */
+int lt_runner_reset(int device);
+int lt_runner_generation(int device);
 
 /* ---- (B) feature extraction --------------------------------------------
  * Replaces extract_features / analyze_program / statement_features
@@ -116,7 +128,7 @@ typedef struct {
   double first_us;      /* warm-up run */
   float max_rel_err;    /* worst relative error over checked outputs (inf if NaN) */
   int32_t repeats;
-  int32_t status;       /* 0 ok, 1 launch refused (resources), 2 kernel fault */
+  int32_t status;       /* 0 ok, 1 launch refused (resources), 2 kernel fault (reset the runner context) */
   char detail[200];
 } lt_measure_record;
 
@@ -126,12 +138,14 @@ int64_t lt_module_function(int64_t module, const char* name);
 int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads, int* static_smem);
 int64_t lt_task_create(int device);
 void lt_task_destroy(int64_t task);
-void lt_task_abandon(int64_t task);      /* host record only, after lt_device_reset */
+void lt_task_abandon(int64_t task);      /* host record only, after lt_runner_reset */
 void* lt_task_stream(int64_t task);
 int lt_task_slot(int64_t task, int slot, int64_t bytes);
 int64_t lt_task_slot_ptr(int64_t task, int slot);
 int lt_task_upload(int64_t task, int slot, const void* host, int64_t bytes);
 int lt_task_download(int64_t task, int slot, void* host, int64_t bytes);
+/* fill n 32-bit words of a slot with `value`, stream-ordered (NaN-poisoning scratch) */
+int lt_task_fill(int64_t task, int slot, int64_t n, uint32_t value);
 int lt_task_run(int64_t task, const lt_launch* launches, int n);
 int lt_measure(int64_t task, const lt_launch* launches, int n_launch, const int32_t* check_pairs,
                const int64_t* numel, int n_check, int min_repeat, int max_repeat, double min_ms,

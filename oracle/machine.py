@@ -21,8 +21,8 @@ import numpy as np
 
 from oracle import features as OF
 from oracle import interp as OI
-from paper_2006_06762_b200.state import ir as IR
-from paper_2006_06762_b200.state.graph import ComputeDAG
+from paper_2006_06762_b200 import state as IR
+from paper_2006_06762_b200.state import ComputeDAG
 
 VALID, INVALID, TIMEOUT = "valid", "invalid", "timeout"
 FULL_CHECK_VOLUME = 1 << 25

@@ -8,6 +8,7 @@
 #include <stdint.h>
 #include <string>
 #include <mutex>
+#include <unistd.h>
 #include "common.h"
 
 extern "C" int lt_features_device(const int32_t*, const int64_t*, int64_t, double*, int*, void*);
@@ -16,10 +17,13 @@ extern "C" int lt_cols_to_rows_device(const double*, int64_t, double*, void*);
 extern "C" int lt_predict_rows_device(int64_t, const double*, int64_t, double*, void*);
 extern "C" int lt_predict_cols_device(int64_t, const double*, int64_t, double*, void*);
 extern "C" int lt_segment_sum_device(const double*, const int64_t*, int64_t, double*, void*);
+extern "C" int lt_runner_reset(int);
+extern "C" int lt_runner_generation(int);
+extern "C" int lt_pool_start(int, const char*, double);
+extern "C" void lt_pool_stop(void);
 
 namespace lt {
 
-int g_device_epoch = 0;
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(const std::string& msg) { g_err = msg; return -1; }
@@ -30,13 +34,6 @@ struct Scratch {
   int init() {
     if (!stream && check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream")) return -1;
     return 0;
-  }
-  void forget() {             // after cudaDeviceReset: the pointers are gone, do not free
-    for (DevBuf* b : {&words, &stmt_off, &rows, &cols, &row_scores, &prog_off, &scores, &err}) {
-      b->ptr = nullptr;
-      b->cap = 0;
-    }
-    stream = nullptr;
   }
   void release() {
     for (DevBuf* b : {&words, &stmt_off, &rows, &cols, &row_scores, &prog_off, &scores, &err}) {
@@ -153,18 +150,33 @@ int lt_score_batch(int64_t model, const int32_t* words, const int64_t* stmt_off,
   return lt::check_cuda(cudaStreamSynchronize(s.stream), "score copy-back");
 }
 
-// Recover from a faulted (sticky-error) context: reset the device and forget
-// every device pointer and per-function attribute this library cached.  Task,
-// module, model and training handles created before become invalid.
-int lt_device_reset(int device) {
+// Library setup: check the devices, create each device's runner context and
+// start the compile pool (n_workers <= 0: host cores - 1) on `cache_dir`
+// (NULL or "": no on-disk cubin cache).
+int lt_init(int n_gpus, const char* cache_dir, int n_workers) {
+  int n = lt_device_count();
+  if (n_gpus < 1 || n_gpus > n) return lt::fail("lt_init: " + std::to_string(n_gpus) + " GPUs asked, " +
+                                                std::to_string(n) + " visible");
+  for (int d = 0; d < n_gpus; ++d)
+    if (lt_runner_generation(d) < 0) return lt::fail("lt_init: bad device");
+  if (n_workers <= 0) {
+    long c = sysconf(_SC_NPROCESSORS_ONLN);
+    n_workers = c > 1 ? (int)c - 1 : 1;
+  }
+  return lt_pool_start(n_workers, cache_dir, 120.0);
+}
+
+// Library teardown, before process exit: stop the compile pool (joins its
+// dispatcher thread and reaps the workers), destroy every runner context (task
+// buffers and candidate modules go with them) and free the scoring scratch.
+// Model and training handles stay valid until their destroy calls.
+int lt_shutdown(void) {
+  lt_pool_stop();
+  int n = lt_device_count();
+  for (int d = 0; d < n; ++d) lt_runner_reset(d);
   std::lock_guard<std::mutex> g(lt::g_mu);
-  cudaSetDevice(device);
-  cudaError_t e = cudaDeviceReset();
-  lt::g_s.forget();
-  lt::runner_forget();
-  ++lt::g_device_epoch;
-  cudaGetLastError();
-  return lt::check_cuda(e, "cudaDeviceReset");
+  lt::g_s.release();
+  return 0;
 }
 
 void lt_release_scratch(void) {

@@ -17,8 +17,6 @@ inline int check_cuda(cudaError_t e, const char* what) {
 }
 inline int check_launch(const char* what) { return check_cuda(cudaGetLastError(), what); }
 
-// incremented by lt_device_reset(): per-function attributes set once per epoch
-extern int g_device_epoch;
 void runner_forget();       // drop cached per-function state (runner.cu)
 
 // Feature columns kept raw (reference src/features.py:74-78): position one-hots of the

@@ -169,17 +169,15 @@ static int predict_device(int64_t handle, const double* d_rows, int64_t n_rows, 
   if (!m) return lt::fail("null model");
   if (n_rows <= 0) return 0;
   size_t smem = (size_t)lt::ROWS_PER_BLOCK * (m->n_used + 1) * sizeof(double);
-  static size_t configured = 0;
-  static int epoch = -1;
-  if (epoch != lt::g_device_epoch) {
-    configured = 0;
-    epoch = lt::g_device_epoch;
-  }
-  if (smem > 48 * 1024 && smem > configured) {
+  // the opt-in shared-memory grant is per device (function attributes are per context)
+  static size_t configured[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > 48 * 1024 && (dev < 0 || dev >= 64 || smem > configured[dev])) {
     if (lt::check_cuda(cudaFuncSetAttribute(lt::predict_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem), "smem attr"))
       return -1;
-    configured = smem;
+    if (dev >= 0 && dev < 64) configured[dev] = smem;
   }
   int64_t blocks = (n_rows + lt::ROWS_PER_BLOCK - 1) / lt::ROWS_PER_BLOCK;
   lt::predict_rows_kernel<<<(unsigned)blocks, lt::ROWS_PER_BLOCK, smem, (cudaStream_t)stream>>>(

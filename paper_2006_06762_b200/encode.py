@@ -38,7 +38,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .state.expr import kind, op_counts, reads
+from .state import kind, op_counts, reads
 
 HDR = 18
 OP_VAR, OP_CONST, OP_ADD, OP_MUL, OP_DIV, OP_MOD = range(6)

@@ -35,6 +35,7 @@ class DeviceMatrix:
         X = np.ascontiguousarray(X, dtype=np.float64)
         self.n, self.nf = X.shape
         self.h = self.lib.lt_gbdt_create(rt.ptr(X, rt.c_f64p), self.n, self.nf)
+        self.epoch = rt.epoch
         if not self.h:
             raise rt.NativeError(f"lt_gbdt_create: {self.lib.lt_last_error().decode()}")
 
@@ -57,15 +58,18 @@ class DeviceMatrix:
                     right[:k].astype(np.int64), val[:k].copy(), 1.0)
 
     def close(self):
-        if self.h:
+        if self.h and self.epoch == rt.epoch:     # after rt.shutdown() the library is torn down
             self.lib.lt_gbdt_destroy(self.h)
-            self.h = 0
+        self.h = 0
 
     def __del__(self):
         try:
             self.close()
         except Exception:
             pass
+
+
+MAX_DEPTH = 7       # csrc/gbdt.cu GB_MAX_FRONTIER = 64 nodes per level
 
 
 _LAST: list = [None, None]      # (weakref to the host matrix, DeviceMatrix)
@@ -104,6 +108,8 @@ def train(records, hyper=None) -> GpuCostModel:
     """`train(records, hyper)` (src/model.py:275): records with y > 0 and
     attached features; returns a GpuCostModel equal to the reference's model."""
     hyper = hyper if hyper is not None else Hyper()
+    if not 1 <= hyper.depth <= MAX_DEPTH:
+        raise ValueError(f"gbdt.train fits trees of depth 1..{MAX_DEPTH} on the device (got {hyper.depth})")
     usable = [r for r in records if r.y > 0]
     if not usable:
         raise ValueError("training needs at least one record with positive throughput")

@@ -222,8 +222,9 @@ def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_fea
     """Rebind the reference's hot-path call sites; returns the originals.
 
     gpu_train: `train` fits its trees on the GPU (`gbdt.train`, bit-identical
-    models); False keeps the reference's own `train` and
-    only wraps its result."""
+    models; trees deeper than `gbdt.MAX_DEPTH` — the
+    device kernel's frontier limit — are fitted by the reference's own `train`);
+    False keeps the reference's own `train` and only wraps its result."""
     import importlib
     sched = importlib.import_module(loomtune.__name__ + ".sched")
     cli = importlib.import_module(loomtune.__name__ + ".cli")
@@ -233,8 +234,8 @@ def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_fea
     ref_train = sched.train
 
     def train(records, hyper=None):
-        if gpu_train:
-            from . import gbdt
+        from . import gbdt
+        if gpu_train and (hyper is None or hyper.depth <= gbdt.MAX_DEPTH):
             m = gbdt.train(records, hyper)
         else:
             m = GpuCostModel.wrap(ref_train(records, hyper) if hyper is not None else ref_train(records))

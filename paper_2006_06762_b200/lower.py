@@ -43,7 +43,7 @@ import math
 import struct
 from dataclasses import dataclass, field
 
-from .state.expr import kind, reads
+from .state import kind, reads
 
 MAX_THREADS = 1024
 MAX_SMEM = 227 * 1024
@@ -930,5 +930,5 @@ def reference_lowering(dag) -> Lowered:
     """State-free fp64 ground truth of a DAG: one naive fp64 kernel per computed
     node in dependency order (the device analogue of `reference_outputs`,
     `src/interp.py:46-74`)."""
-    from .state.ir import naive_program
+    from .state import naive_program
     return lower(naive_program(dag), dtype="double")

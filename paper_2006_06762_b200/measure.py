@@ -42,7 +42,7 @@ import numpy as np
 from . import runtime as rt
 from .lower import Lowered, LoweringError, lower, reference_lowering
 from .ptxgen import Unsupported, lower_ptx
-from .state.ir import validate
+from .state import validate
 
 VALID, INVALID, TIMEOUT = "valid", "invalid", "timeout"
 GPU_TOL = 1e-4
@@ -215,6 +215,12 @@ class _DagContext:
             b = lo.buffers[name]
             pairs += [self.buffer_slot(b, False), self.slots[f"ref:{name}"]]
             numel.append(b.numel)
+        # intermediate buffers are shared by every candidate of the DAG: NaN-poison
+        # them too, so a candidate cannot pass on values an earlier one left there
+        for b in lo.buffers.values():
+            if b.role == "temp" and b.name not in lo.outputs:
+                rt.check(self.r.lib.lt_task_fill(self.task, self.buffer_slot(b, False), b.numel, 0x7FC00000),
+                         "poison temp")
         pairs_a = np.asarray(pairs, np.int32)
         numel_a = np.asarray(numel, np.int64)
         rec = rt.MeasureRecord()
@@ -319,9 +325,11 @@ class Runner:
         return self._lpool
 
     def reset_device(self) -> None:
-        """After a kernel fault (the context is unusable): reset the device, drop
-        every module and DAG context (re-created on demand) and carry on."""
-        rt.device_reset(self.device)
+        """After a kernel fault (the runner context is unusable): destroy the
+        runner's private context (lt_runner_reset; torch's primary context and
+        the scoring/training state are untouched), drop every module and DAG
+        context (re-created on demand from kept images) and carry on."""
+        rt.runner_reset(self.device)
         with self.mod_lock:
             self.modules.clear()
             self.pinned.clear()
@@ -582,14 +590,11 @@ class Runner:
             print(f"[lt trace] measuring #{i} {key[:12]} {[k.info.get('template') for k in lo.kernels]}",
                   file=sys.stderr, flush=True)
         t0 = time.perf_counter()
-        try:
-            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
-        except rt.NativeError as e:
-            if "kernel fault" not in str(e):
-                raise
+        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        if m.status == 2:
             # a faulting candidate is INVALID like any other failure (SPEC.md:522:
-            # measure_batch never raises); the device is reset and the batch continues
-            rec.detail = "gpu: " + str(e).split(": ", 1)[-1][:200]
+            # measure_batch never raises); the runner context is reset and the batch continues
+            rec.detail = "gpu: " + m.detail.decode(errors="replace")
             self.reset_device()
             return
         self.stats["gpu_s"] += time.perf_counter() - t0
@@ -627,11 +632,8 @@ class Runner:
             return None
         funcs = self.load(key + (":O1" if opts == PTX_SAFE_OPTS else ":O3"), data, entries)
         t0 = time.perf_counter()
-        try:
-            m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
-        except rt.NativeError as e:
-            if "kernel fault" not in str(e):
-                raise
+        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        if m.status == 2:
             self.reset_device()
             return None
         self.stats["gpu_s"] += time.perf_counter() - t0

@@ -31,7 +31,7 @@ from .lower import (
     Lowered, LoweringError, _attached, _binding, _must_materialize, _reads_buffer, _unroll_flags, promote_register_tile,
     _written, ident, tile_levels,
 )
-from .state.expr import kind, reads
+from .state import kind, reads
 
 
 # statements between a shared-memory load and its first use (16-128 measured within 2%
@@ -784,8 +784,8 @@ def _xreduce_pairs(mod: _Mod) -> dict:
     neither stage is attached, and the partial's space loops enumerate
     (rf, space...) in row-major order (checked on sample points, so a State
     whose loops were reordered keeps the two-kernel naive lowering)."""
-    from .state.expr import Lin
-    from .state.ir import d_eval, d_vars
+    from .state import Lin
+    from .state import d_eval, d_vars
     if "xreduce" in _OFF:
         return {}
     p, out = mod.p, {}

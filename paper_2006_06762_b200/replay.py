@@ -5,7 +5,8 @@ logged program and demands the exact logged cost: right for its deterministic
 analytical machine, impossible for measured device time.  `replay_log` keeps
 its contract where it still holds and relaxes it where it cannot:
 
-* the log is read exactly as the reference reads it (`src/logio.py:60-95`): NDJSON,
+* the log is read by the reference's own reader (`loomtune.logio.iter_records`,
+  `src/logio.py:61-88`): NDJSON,
   every record stamped with schema version 1, a truncated or corrupt line or a
   foreign schema raises `LogError` naming the line; the header builds the DAGs
   (`src/cli.py:199-206`);
@@ -27,37 +28,9 @@ from __future__ import annotations
 import json
 import math
 
-SCHEMA_VERSION = 1          # src/logio.py:19
+from .reference import loomtune  # noqa: F401
 
-
-class LogError(Exception):
-    """A log that cannot be read (src/logio.py:22-29)."""
-
-    def __init__(self, message: str, line: int | None = None):
-        if line is not None:
-            message = f"line {line}: {message}"
-        super().__init__(message)
-        self.line = line
-
-
-def iter_records(path: str):
-    """NDJSON records with the reference's damage checks (src/logio.py:60-86)."""
-    with open(path, encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            if not line.strip():
-                continue
-            if not line.endswith("\n"):
-                raise LogError("truncated record (no trailing newline)", lineno)
-            try:
-                rec = json.loads(line)
-            except json.JSONDecodeError as err:
-                raise LogError(f"corrupt record: {err.msg}", lineno) from err
-            if not isinstance(rec, dict):
-                raise LogError("record is not an object", lineno)
-            if rec.get("schema") != SCHEMA_VERSION:
-                raise LogError(f"schema version {rec.get('schema')!r} is not supported "
-                               f"(this reader handles {SCHEMA_VERSION})", lineno)
-            yield rec
+from loomtune.logio import SCHEMA_VERSION, LogError, iter_records  # noqa: E402,F401  (the reference's reader)
 
 
 def load_log(path: str):

@@ -6,6 +6,7 @@ every entry point raises.  ctypes releases the GIL for the duration of each call
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 
@@ -14,7 +15,7 @@ import numpy as np
 from . import build as _build
 
 _lib = None
-epoch = 0       # incremented by device_reset(); handles from an older epoch are dead
+epoch = 0       # incremented by shutdown(): device handles from an older epoch are dead
 
 c_i32p = ctypes.POINTER(ctypes.c_int32)
 c_i64p = ctypes.POINTER(ctypes.c_int64)
@@ -52,8 +53,12 @@ _SIGS = [
     ("lt_score_batch", ctypes.c_int, [ctypes.c_int64, c_i32p, c_i64p, ctypes.c_int64, c_i64p, ctypes.c_int64,
                                       c_f64p, c_f64p]),
     ("lt_release_scratch", None, []),
-    ("lt_device_reset", ctypes.c_int, [ctypes.c_int]),
+    ("lt_init", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
+    ("lt_shutdown", ctypes.c_int, []),
+    ("lt_runner_reset", ctypes.c_int, [ctypes.c_int]),
+    ("lt_runner_generation", ctypes.c_int, [ctypes.c_int]),
     ("lt_task_abandon", None, [ctypes.c_int64]),
+    ("lt_task_fill", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32]),
     # GBDT training (csrc/gbdt.cu)
     ("lt_gbdt_create", ctypes.c_int64, [c_f64p, ctypes.c_int64, ctypes.c_int]),
     ("lt_gbdt_destroy", None, [ctypes.c_int64]),
@@ -131,9 +136,21 @@ def ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(ctype)
 
 
-def device_reset(device: int) -> None:
-    """Recover from a kernel fault: reset the device (lt_device_reset) and bump
-    the epoch so device-side handles (models, scratch) are re-created."""
+def runner_reset(device: int) -> None:
+    """Recover from a kernel fault: destroy the runner's private context on
+    `device` (lt_runner_reset).  Candidate modules and task buffers die with it;
+    the primary context (torch tensors, NCCL, models, training matrices) is
+    untouched."""
+    check(load().lt_runner_reset(device), "runner reset")
+
+
+def shutdown() -> None:
+    """lt_shutdown before interpreter teardown (atexit): compile pool joined,
+    runner contexts destroyed, scratch freed; later handle destructors are no-ops."""
     global epoch
-    check(load().lt_device_reset(device), "device reset")
-    epoch += 1
+    if _lib is not None:
+        epoch += 1
+        _lib.lt_shutdown()
+
+
+atexit.register(shutdown)

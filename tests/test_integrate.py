@@ -1,17 +1,9 @@
 """install(): the reference's unchanged tuner runs on the B200 path."""
 
-import os
-import sys
-
 import numpy as np
 import pytest
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-for cand in ("/root/reference/pkg/src", os.path.join(ROOT, "baseline", "_ref")):
-    if os.path.isdir(os.path.join(cand, "loomtune")):
-        sys.path.insert(0, cand)
-        break
-LT = pytest.importorskip("loomtune")
+from paper_2006_06762_b200.reference import loomtune as LT     # baseline/_ref travels with the repo
 
 
 class CpuBatchModel:

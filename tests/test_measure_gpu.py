@@ -126,26 +126,69 @@ def test_baseline_configs_measure(corpus, runner):
             print("  ", corpus.entries[idx[k]]["dag"], f"{r.cost_us:.1f} us", r.info["kernels"][0].get("template"))
 
 
-def test_device_reset_recovery():
-    """After a kernel fault the runner resets the device (lt_device_reset) and
-    carries on: modules reload from kept cubins, DAG contexts and the cost
-    model's device handle are re-created."""
+FAULT_PTX = b""".version 8.7
+.target sm_100a
+.address_size 64
+.visible .entry lt_fault()
+{
+  .reg .b64 %rd<2>;
+  .reg .b32 %r<2>;
+  mov.u64 %rd1, 16;
+  mov.u32 %r1, 7;
+  st.global.u32 [%rd1], %r1;
+  ret;
+}
+"""
+
+
+def test_kernel_fault_is_contained_in_the_runner_context():
+    """A faulting candidate (illegal address) poisons only the runner's private
+    context: lt_measure reports status 2 (INVALID), lt_runner_reset destroys that
+    context, torch tensors and the cost model's device state in the primary
+    context stay valid, and measurement carries on (modules reload from kept
+    images, DAG contexts are re-created)."""
+    import ctypes
     import numpy as np
+    import torch
     from paper_2006_06762_b200 import measure
+    from paper_2006_06762_b200 import runtime as rt
     from paper_2006_06762_b200.model import GpuCostModel
     from paper_2006_06762_b200.state import build, naive_program
     r = measure.configure(device=0, cache_dir="")
-    dag = build("matmul", n=64, m=64, k=64)
-    p = naive_program(dag)
-    (a,) = r.measure_programs([p])
-    m = GpuCostModel(base=1.0)
-    s0 = m.predict_batch([p])
-    r.reset_device()
-    assert r.stats["device_resets"] == 1
-    (b,) = r.measure_programs([p])          # same kernel: reloaded from the kept cubin
-    assert a.status == b.status == "valid"
-    assert np.array_equal(m.predict_batch([p]), s0)
-    measure._shutdown()
+    try:
+        dag = build("matmul", n=64, m=64, k=64)
+        p = naive_program(dag)
+        (a,) = r.measure_programs([p])
+        assert a.status == "valid"
+        x = torch.arange(1 << 20, dtype=torch.float32, device="cuda")
+        m = GpuCostModel(base=1.0)
+        s0 = m.predict_batch([p])
+        gen0 = r.lib.lt_runner_generation(0)
+        mod = r.lib.lt_module_load(0, FAULT_PTX, len(FAULT_PTX))
+        assert mod, r.lib.lt_last_error()
+        fn = r.lib.lt_module_function(mod, b"lt_fault")
+        task = r.context(dag, 0).task
+        launches = (rt.Launch * 1)()
+        launches[0].func = fn
+        launches[0].grid[:] = (1, 1, 1)
+        launches[0].block[:] = (32, 1, 1)
+        launches[0].n_args = 0
+        rec = rt.MeasureRecord()
+        empty_i = np.zeros(1, np.int32)
+        empty_l = np.zeros(1, np.int64)
+        rt.check(r.lib.lt_measure(task, ctypes.addressof(launches), 1, rt.ptr(empty_i, rt.c_i32p),
+                                  rt.ptr(empty_l, rt.c_i64p), 0, 1, 5, 1.0, ctypes.addressof(rec)), "lt_measure")
+        assert rec.status == 2 and b"kernel fault" in rec.detail
+        r.reset_device()
+        assert r.lib.lt_runner_generation(0) == gen0 + 1
+        assert r.stats["device_resets"] == 1
+        torch.cuda.synchronize()                                  # the primary context is healthy
+        assert float(x[-1]) == float((1 << 20) - 1)
+        assert np.array_equal(m.predict_batch([p]), s0)
+        (b,) = r.measure_programs([p])          # same kernel: reloaded from the kept image
+        assert b.status == "valid"
+    finally:
+        measure._shutdown()
 
 
 def test_naive_multi_point_steps_verify():

@@ -10,8 +10,8 @@ import pytest
 
 from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
 from paper_2006_06762_b200.state import workloads as W
-from paper_2006_06762_b200.state.expr import Lin, Read, Reduce
-from paper_2006_06762_b200.state.graph import compute, placeholder
+from paper_2006_06762_b200.state import Lin, Read, Reduce
+from paper_2006_06762_b200.state import compute, placeholder
 
 
 def rfactor_history(stage, red, factor, space, pragma=64, annotate=True):
@@ -77,7 +77,7 @@ def test_reordered_partial_keeps_the_naive_lowering():
     from paper_2006_06762_b200.ptxgen import lower_ptx
     dag = rows_dag(48, 64, "sum")
     h = list(rfactor_history("r", ["j"], 8, ["u"], annotate=False))
-    from paper_2006_06762_b200.state.ir import Reorder
+    from paper_2006_06762_b200.state import Reorder
     h.insert(-1, Reorder("r.rf", ("u", "rf", "rk")))
     lo = lower_ptx(replay(dag, tuple(h)))
     assert [k.info["template"] for k in lo.kernels] == ["naive", "naive"]
