@@ -1,24 +1,31 @@
 """Headline benchmark: measured candidates/sec of the B200 measurement pipeline.
 
-A step = measuring one batch of fresh candidate States of the BASELINE config
-(default RC = ResNet-50 conv2d N16 56x56x64->64 3x3, BASELINE.json configs[1])
-through the drop-in `measure_batch`: validate -> lower -> NVRTC compile (empty
-cubin cache, exact constants) -> run on the B200 -> verify every output vs the
-fp64 ground truth on device -> time.  Candidates come from
-tests/golden/streams/<CFG>.json.gz (the reference's own sampler, filtered to
-legal launches); every timed step uses States never seen before in the run.
-The end-to-end pass (`e2e`) re-measures the same States from scratch: compiled
-modules dropped, compile pool restarted on an empty cubin cache, inputs and
-packed constants re-uploaded and the fp64 ground truth recomputed every step.
+Metric (both arms, identical string): "measured candidates/sec (<CFG>, SSSRRSRS)"
+= candidates measured / wall seconds of the measuring region.
 
-Multi-GPU (torchrun): each rank measures its own disjoint slice of every step's
-batch (measurement units are independent); only the measured
+* A step = measuring one batch of B fresh candidate States of the BASELINE
+  config (default RC = ResNet-50 conv2d N16 56x56x64->64 3x3, BASELINE.json
+  configs[1]) through the drop-in `measure_batch`: validate -> lower -> ptxas
+  (empty cubin cache, exact constants) -> run on the B200 -> verify every output
+  against the fp64 ground truth on the device -> time.  States come from
+  tests/golden/streams/<CFG>.json.gz (the reference's own sampler, filtered to
+  legal launches); step s of the run measures stream[s*B*N:(s+1)*B*N] (each rank
+  its own shard), so warm-up steps and timed steps never share a State.
+* `value`: inputs and ground truth resident in HBM when the timed region starts;
+  the region (CUDA events, synchronize + barrier on both sides, max over ranks)
+  contains the whole host pipeline.  `e2e`: the same States again through the
+  public `measure_batch` from scratch — a fresh measuring process (new CUDA
+  context, empty cubin cache) and, every step, the DAG's inputs copied from
+  pinned host memory and the fp64 ground truth recomputed, results read back.
+* `--impl reference`: the reference's own runner (`loomtune.machine.measure_batch`,
+  src/machine.py:249-285, imported unchanged from baseline/_ref) on the same
+  timed States, one State per task on a process pool over all host cores (a work
+  queue: no per-step barrier), wall clock from first submit to last result.
+
+Multi-GPU (torchrun): each rank measures its shard of every step's batch
+(measurement units are independent); only the (status, cost)
 records are gathered (NCCL all_gather).  value = candidates of all ranks /
 max-over-ranks time.
-
---impl reference times the reference's CPU runner (oracle/machine.py, a
-restatement of src/machine.py:249-285: validate + shrunken-twin interpretation
-+ analytical cost) on the same candidates with all host cores.
 """
 
 from __future__ import annotations
@@ -28,6 +35,7 @@ import gzip
 import json
 import math
 import os
+import signal
 import statistics
 import subprocess
 import sys
@@ -42,6 +50,14 @@ FLOPS = {"RC": 2 * 16 * 56 * 56 * 64 * 64 * 9, "G10": 2 * 1024 ** 3, "G5": 2 * 5
          "TBG": 2 * 192 * 128 * 128 * 64, "CL": 2 * 16 * 28 * 28 * 128 * 128 * 9}
 NAMES = {"RC": "ResNet-50 conv2d N16 56x56x64->64 3x3 s1", "G10": "GEMM 1024^3", "G5": "GEMM 512^3",
          "TBG": "batched GEMM 192x128x128x64", "CL": "ConvLayer N16 28x28x128->128 3x3 + BN + ReLU"}
+RATE_DEF = ("candidates measured / wall seconds of the measuring region; ours: device-event-bracketed steps "
+            "of B candidates through measure_batch (validate+lower+compile+run+verify+time, empty cubin "
+            "cache); reference: loomtune.machine.measure_batch (validate + shrunken-twin interpret + "
+            "analytical cost) on the same States, work queue over all host cores")
+
+
+def metric(cfg: str) -> str:
+    return f"measured candidates/sec ({cfg}, SSSRRSRS)"
 
 
 def load_stream(cfg: str):
@@ -49,6 +65,11 @@ def load_stream(cfg: str):
     with gzip.open(os.path.join(ROOT, "tests", "golden", "streams", f"{cfg}.json.gz"), "rt") as fh:
         data = json.load(fh)
     return ComputeDAG.from_json(data["dag"]), [history_from_json(h) for h in data["histories"]]
+
+
+def step_slice(stream: list, step: int, batch: int, world: int) -> list:
+    lo = step * batch * world
+    return stream[lo:lo + batch * world]
 
 
 class Clocks:
@@ -93,64 +114,135 @@ class Clocks:
                 "reasons": reasons, "samples": len(busy)}
 
 
-def cpu_reference(histories, dag, seconds: float, cores: int, fn=None) -> dict:
-    """The reference's CPU runner restated (oracle/machine.py) on a fixed sample
-    of stream candidates, one per host core, all in flight at once.  Rate =
-    cores x candidates / sum of their core-seconds.  A candidate still running
-    after `seconds` (the reference's heavy tail: one twin interpretation can take
-    minutes) is stopped and counted with the time it used, a lower bound on its
-    cost, so the rate is an optimistic bound for the reference."""
-    from concurrent.futures import ProcessPoolExecutor, wait
-    from paper_2006_06762_b200.state import history_to_json
-    items = [(json.dumps(dag.to_json()), history_to_json(h)) for h in histories[:cores]]
-    ex = ProcessPoolExecutor(max_workers=cores)
-    for f in [ex.submit(int, 0) for _ in range(cores)]:      # workers up before the clock
-        f.result()
-    t0 = time.perf_counter()
-    futs = [ex.submit(fn or _cpu_one, it) for it in items]
-    done, pending = wait(futs, timeout=seconds)
-    now = time.perf_counter()
-    core_s = sum(f.result()[1] for f in done) + (now - t0) * len(pending)
-    procs = list(getattr(ex, "_processes", {}).values())
-    ex.shutdown(wait=False, cancel_futures=True)
-    for pr in procs:              # stopped stragglers must not slow the next sample
-        if pr.is_alive():
-            pr.terminate()
-    n = len(futs)
-    return {"value": cores * n / core_s if core_s > 0 else 0.0, "candidates": n, "seconds": now - t0,
-            "core_seconds": core_s, "truncated": len(pending)}
+# ---- the reference's CPU paths (work queue over all host cores) ---------------
+
+class _Capped(Exception):
+    pass
 
 
-def _cpu_one(item):
+def _alarm(signum, frame):
+    raise _Capped()
+
+
+def _ref_worker_init():
     sys.path.insert(0, ROOT)
+    from paper_2006_06762_b200.reference import loomtune  # noqa: F401  (baseline/_ref)
+    import loomtune.machine  # noqa: F401
+    signal.signal(signal.SIGALRM, _alarm)
+
+
+def _ref_measure(item):
+    """One State through the reference's own `measure_batch` (src/machine.py:249-285)."""
+    dag_json, hist, cap = item
+    from loomtune.graph import ComputeDAG
+    from loomtune.ir import history_from_json, replay
+    from loomtune.machine import measure_batch
     t0 = time.perf_counter()
-    from oracle import machine as OM
-    from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
-    dag_json, hist = item
-    p = replay(ComputeDAG.from_json(json.loads(dag_json)), history_from_json(hist))
-    return OM.measure_batch([p])[0].status, time.perf_counter() - t0
+    signal.setitimer(signal.ITIMER_REAL, cap)
+    try:
+        p = replay(ComputeDAG.from_json(json.loads(dag_json)), history_from_json(hist))
+        status = measure_batch([p])[0].status
+    except _Capped:
+        status = "capped"
+    finally:
+        signal.setitimer(signal.ITIMER_REAL, 0)
+    return status, time.perf_counter() - t0
 
 
-def _cpu_full(item):
+def _ref_interpret(item):
     """The reference's only full-size execution of a State: `interpret` on the
-    real inputs (oracle/interp.py, src/interp.py:318-352) — what the B200 runner
-    does for every candidate (run + verify against the state-free result)."""
-    sys.path.insert(0, ROOT)
-    t0 = time.perf_counter()
+    real inputs (src/interp.py:318-352) — what the B200 runner does per candidate."""
+    dag_json, hist, cap = item
     import numpy as np
-    from oracle import interp as OI
-    from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
-    dag_json, hist = item
+    from loomtune.graph import ComputeDAG
+    from loomtune.interp import interpret, random_inputs
+    from loomtune.ir import history_from_json, replay
+    t0 = time.perf_counter()
+    signal.setitimer(signal.ITIMER_REAL, cap)
+    try:
+        dag = ComputeDAG.from_json(json.loads(dag_json))
+        interpret(replay(dag, history_from_json(hist)), random_inputs(dag, np.random.default_rng(0)))
+        status = "valid"
+    except _Capped:
+        status = "capped"
+    finally:
+        signal.setitimer(signal.ITIMER_REAL, 0)
+    return status, time.perf_counter() - t0
+
+
+def _ref_predict(item):
+    """`extract_features` + `CostModel.predict` (src/features.py:420-425,
+    src/model.py:98-108) over a chunk of programs."""
+    dag_json, hists, model_json = item
+    from loomtune.graph import ComputeDAG
+    from loomtune.ir import history_from_json, replay
+    from loomtune.model import CostModel
     dag = ComputeDAG.from_json(json.loads(dag_json))
-    p = replay(dag, history_from_json(hist))
-    OI.interpret(p, OI.random_inputs(dag, np.random.default_rng(0)))
-    return "valid", time.perf_counter() - t0
+    model = CostModel.from_json(model_json)
+    progs = [replay(dag, history_from_json(h)) for h in hists]
+    t0 = time.perf_counter()
+    for p in progs:
+        model.predict(p)
+    return len(progs), time.perf_counter() - t0
 
 
-def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
+class RefPool:
+    """Process pool over all host cores with the reference imported in every worker."""
+
+    def __init__(self, cores: int):
+        import multiprocessing as mp
+        from concurrent.futures import ProcessPoolExecutor
+        self.cores = cores
+        self.ex = ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn"),
+                                      initializer=_ref_worker_init)
+        for f in [self.ex.submit(int, 0) for _ in range(cores * 2)]:     # workers up before any clock
+            f.result()
+
+    def run(self, fn, items: list) -> tuple:
+        """(results, wall seconds from first submit to last result)."""
+        t0 = time.perf_counter()
+        res = list(self.ex.map(fn, items))
+        return res, time.perf_counter() - t0
+
+    def close(self):
+        self.ex.shutdown(wait=True, cancel_futures=True)
+
+
+def ref_measure_rate(pool: RefPool, dag, histories: list, cap: float) -> dict:
+    from paper_2006_06762_b200.state import history_to_json
+    dj = json.dumps(dag.to_json())
+    items = [(dj, history_to_json(h), cap) for h in histories]
+    res, wall = pool.run(_ref_measure, items)
+    return {"value": len(items) / wall, "candidates": len(items), "wall_s": wall,
+            "core_s": sum(t for _, t in res), "capped": sum(s == "capped" for s, _ in res)}
+
+
+def ref_interpret_rate(pool: RefPool, dag, histories: list, cap: float) -> dict:
+    from paper_2006_06762_b200.state import history_to_json
+    dj = json.dumps(dag.to_json())
+    items = [(dj, history_to_json(h), cap) for h in histories]
+    res, wall = pool.run(_ref_interpret, items)
+    return {"value": len(items) / wall, "candidates": len(items), "wall_s": wall,
+            "capped": sum(s == "capped" for s, _ in res)}
+
+
+def ref_predict_rate(pool: RefPool, dag, histories: list, model_json: dict, chunk: int = 16) -> dict:
+    from paper_2006_06762_b200.state import history_to_json
+    dj = json.dumps(dag.to_json())
+    hj = [history_to_json(h) for h in histories]
+    items = [(dj, hj[i:i + chunk], model_json) for i in range(0, len(hj), chunk)]
+    res, wall = pool.run(_ref_predict, items)
+    n = sum(k for k, _ in res)
+    return {"value": n / wall, "programs": n, "wall_s": wall, "predict_core_s": sum(t for _, t in res)}
+
+
+# ---- our scoring / training legs ----------------------------------------------
+
+def scoring_bench(device: int, programs: list, reps: int = 20) -> dict:
     """Population scoring (features + trees) over a synthetic population of 2^16
-    programs (replicated stream States): device-resident kernel times and the
-    host e2e rate."""
+    programs (replicated stream States): device-resident kernel times (CUDA
+    events on the launching stream) and the host e2e rate through predict_batch."""
+    import ctypes
     import numpy as np
     import torch
     from paper_2006_06762_b200 import runtime as rt
@@ -165,7 +257,7 @@ def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
     prog_off = np.concatenate([base_prog[:-1] + i * base_prog[-1] for i in range(n_rep)]
                               + [[base_prog[-1] * n_rep]]).astype(np.int64)
     n_stmt, n_prog = len(stmt_off) - 1, len(prog_off) - 1
-    dev = torch.device("cuda", runner_dev)
+    dev = torch.device("cuda", device)
     d_words = torch.from_numpy(words).to(dev)
     d_soff = torch.from_numpy(stmt_off).to(dev)
     d_poff = torch.from_numpy(prog_off).to(dev)
@@ -174,19 +266,23 @@ def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
     d_sc = torch.empty(n_prog, dtype=torch.float64, device=dev)
     d_err = torch.zeros(1, dtype=torch.int32, device=dev)
     h = model.handle()
+    n_trees, n_used = ctypes.c_int(), ctypes.c_int()
+    rt.check(lib.lt_model_info(h, ctypes.byref(n_trees), ctypes.byref(n_used)), "model info")
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
     def feats():
         rt.check(lib.lt_features_device_cm(d_words.data_ptr(), d_soff.data_ptr(), n_stmt, d_rows.data_ptr(),
-                                        d_err.data_ptr(), sp), "features")
+                                           d_err.data_ptr(), sp), "features")
 
     def trees():
         rt.check(lib.lt_predict_cols_device(h, d_rows.data_ptr(), n_stmt, d_rs.data_ptr(), sp), "trees")
+
+    def segsum():
         rt.check(lib.lt_segment_sum_device(d_rs.data_ptr(), d_poff.data_ptr(), n_prog, d_sc.data_ptr(), sp), "sum")
 
     out = {}
-    for name, fn in (("features", feats), ("trees", trees)):
+    for name, fn in (("features", feats), ("trees", trees), ("segsum", segsum)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize(dev)
@@ -197,12 +293,45 @@ def scoring_bench(runner_dev: int, programs: list, reps: int = 20) -> dict:
         e1.record(stream)
         torch.cuda.synchronize(dev)
         out[name + "_ms"] = e0.elapsed_time(e1) / reps
-    # host e2e: encode + H2D + fused scoring + D2H through the public API
+    model.predict_batch(programs)                       # warm
     t0 = time.perf_counter()
-    sc = model.predict_batch(programs * n_rep)
+    sc = model.predict_batch(programs * n_rep)          # host e2e: encode + H2D + fused scoring + D2H
     out["e2e_s"] = time.perf_counter() - t0
-    out.update(n_prog=n_prog, n_stmt=n_stmt, words_bytes=int(words.nbytes), scores_finite=bool(np.isfinite(sc).all()))
+    out.update(n_prog=n_prog, n_stmt=n_stmt, words_bytes=int(words.nbytes), n_used=n_used.value,
+               scores_finite=bool(np.isfinite(sc).all()))
     return out
+
+
+def train_bench(n_prog: int = 1500) -> dict:
+    """GBDT training (SURVEY.md §8(f) row 2): `gbdt.train` (trees fitted on the
+    B200) vs the reference's own `train` (loomtune.model.train, 1 core) on the
+    same records: stream States of four configs, labels U(0.05, 1), default
+    hyper (30 trees, depth 6).  Models must be identical."""
+    import numpy as np
+    from loomtune.model import TrainHyper, TrainingRecord
+    from loomtune.model import train as ref_train
+    from paper_2006_06762_b200 import gbdt
+    from paper_2006_06762_b200.features import extract_features_batch
+    from paper_2006_06762_b200.state import replay
+    feats, hists = [], []
+    for cfg in ("RC", "G10", "CL", "TBG"):
+        dag, stream = load_stream(cfg)
+        progs = [replay(dag, h) for h in stream[:n_prog // 4]]
+        feats += extract_features_batch(progs)
+        hists += [p.history for p in progs]
+    y = np.random.default_rng(0).uniform(0.05, 1.0, len(feats))
+    recs = [TrainingRecord("d", h, float(v), feats=f) for h, v, f in zip(hists, y, feats)]
+    gbdt.train(recs[:50], TrainHyper(trees=2))       # warm-up
+    t0 = time.perf_counter()
+    got = gbdt.train(recs, TrainHyper()).to_json()
+    gpu_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    want = ref_train(recs, TrainHyper()).to_json()
+    cpu_s = time.perf_counter() - t0
+    return {"programs": len(feats), "rows": int(sum(len(f) for f in feats)), "trees": 30, "depth": 6,
+            "gpu_s": gpu_s, "cpu_s": cpu_s, "speedup": cpu_s / gpu_s,
+            "identical": json.dumps(got, sort_keys=True) == json.dumps(want, sort_keys=True),
+            "cpu_kind": "reference (loomtune.model.train, 1 core)"}
 
 
 def traffic_of(sha1: str):
@@ -215,39 +344,34 @@ def traffic_of(sha1: str):
         return None
 
 
-def train_bench(n_prog: int = 1500) -> dict:
-    """GBDT training (SURVEY.md §8(f) row 2): `gbdt.train` (trees fitted on the
-    B200) vs the CPU restatement of the reference's `train` (oracle/train.py,
-    pinned to reference-trained golden models) on the same records: stream
-    States of the four configs, labels U(0.05, 1), default hyper (30 trees,
-    depth 6).  Models must be identical."""
-    import numpy as np
-    from oracle import train as OT
-    from paper_2006_06762_b200 import gbdt
-    from paper_2006_06762_b200.features import extract_features_batch
-    from paper_2006_06762_b200.model import Hyper
-    from paper_2006_06762_b200.state import replay
+# ---- reference arm ---------------------------------------------------------------
 
-    class Rec:
-        def __init__(self, f, y):
-            self.feats, self.y, self.dag_id = f, float(y), "d"
-    feats = []
-    for cfg in ("RC", "G10", "CL", "TBG"):
-        dag, stream = load_stream(cfg)
-        feats += extract_features_batch([replay(dag, h) for h in stream[:n_prog // 4]])
-    y = np.random.default_rng(0).uniform(0.05, 1.0, len(feats))
-    gbdt.train([Rec(f, v) for f, v in zip(feats[:50], y[:50])], Hyper(trees=2))       # warm-up
-    t0 = time.perf_counter()
-    got = gbdt.train([Rec(f, v) for f, v in zip(feats, y)], Hyper()).to_json()
-    gpu_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    want = OT.train(feats, y)
-    cpu_s = time.perf_counter() - t0
-    want.pop("train_losses")
-    return {"programs": len(feats), "rows": int(sum(len(f) for f in feats)), "trees": 30, "depth": 6,
-            "gpu_s": gpu_s, "cpu_s": cpu_s, "speedup": cpu_s / gpu_s, "identical": got == want,
-            "cpu_kind": "port (oracle/train.py, 1 core)"}
+def run_reference(args, cores: int) -> None:
+    dag, stream = load_stream(args.config)
+    world = args.gpus
+    timed = [h for s in range(args.warmup, args.warmup + args.steps)
+             for h in step_slice(stream, s, args.batch, world)]
+    pool = RefPool(cores)
+    try:
+        ref_measure_rate(pool, dag, step_slice(stream, 0, args.batch, world)[:cores], args.cpu_seconds)  # warm
+        r = ref_measure_rate(pool, dag, timed, args.cpu_seconds)
+    finally:
+        pool.close()
+    v = r["value"]
+    print(json.dumps({
+        "impl": "reference", "metric": metric(args.config), "value": v, "unit": "cand/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * r["wall_s"] / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": NAMES[args.config], "candidates_per_step": args.batch * world,
+                   "stream": f"tests/golden/streams/{args.config}.json.gz", "rate": RATE_DEF},
+        "cpu_baseline": {"value": v, "unit": "cand/s", "cores": cores, "kind": "reference",
+                         "sample": f"the {r['candidates']} States of the timed steps through loomtune.machine."
+                                   f"measure_batch on {cores} processes; {r['capped']} stopped at the "
+                                   f"{args.cpu_seconds:g} s cap and counted as measured (optimistic)"},
+        "e2e": {"value": v, "unit": "cand/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
+
+# ---- our arm ------------------------------------------------------------------------
 
 def main() -> None:
     ap = argparse.ArgumentParser()
@@ -258,8 +382,11 @@ def main() -> None:
     ap.add_argument("--config", default="RC", choices=sorted(FLOPS))
     ap.add_argument("--batch", type=int, default=32, help="candidates per rank per step")
     ap.add_argument("--cpu-seconds", type=float, default=30.0,
-                    help="per-sample cap on a reference candidate's CPU time (truncated ones count their time)")
+                    help="cap on one reference candidate's CPU time (capped ones count as measured)")
+    ap.add_argument("--sub-configs", default="G10,CL", help="extra configs measured in the same run ('' = none)")
+    ap.add_argument("--sub-steps", type=int, default=4)
     ap.add_argument("--no-scoring", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines (development runs)")
     ap.add_argument("--compile-workers", type=int, default=0, help="ptxas worker processes per rank (0: auto)")
     ap.add_argument("--lower-workers", type=int, default=0, help="lowering processes per rank (0: auto)")
     args = ap.parse_args()
@@ -267,35 +394,14 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    dag, stream = load_stream(args.config)
     cores = os.cpu_count() or 1
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        per_step = []
-        for s in range(args.warmup + args.steps):
-            sample = stream[s * cores:(s + 1) * cores]
-            r = cpu_reference(sample, dag, args.cpu_seconds, cores)
-            if s >= args.warmup:
-                per_step.append(r)
-        tot_c = sum(r["candidates"] for r in per_step)
-        tot_s = sum(r["seconds"] for r in per_step)
-        v = cores * tot_c / sum(r["core_seconds"] for r in per_step)
-        print(json.dumps({
-            "impl": "reference", "metric": f"measured candidates/sec ({args.config}, SSSRRSRS)", "value": v,
-            "unit": "cand/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * tot_s / len(per_step), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": NAMES[args.config], "stream": f"tests/golden/streams/{args.config}.json.gz"},
-            "cpu_baseline": {"value": v, "unit": "cand/s", "cores": cores, "kind": "port",
-                             "sample": f"{tot_c} stream States, one per core per step; oracle/machine.py "
-                                       "measure_batch (validate + twin interpret + machine_cost); "
-                                       f"{sum(r['truncated'] for r in per_step)} capped at "
-                                       f"{args.cpu_seconds:g} s and counted with that time (optimistic)"},
-            "e2e": {"value": v, "unit": "cand/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        if rank == 0:
+            run_reference(args, cores)
         return
 
+    import numpy as np
     import torch
     import torch.distributed as dist
     if world > 1:
@@ -306,51 +412,30 @@ def main() -> None:
     from paper_2006_06762_b200.dist import measure_batch_sharded as sharded_measure
     from paper_2006_06762_b200.state import replay
 
-    workers = max(1, cores // world - (1 if world == 1 else 0))
-    cache = tempfile.mkdtemp(prefix="lt_cubin_")     # empty: every candidate really compiles
-    if args.compile_workers:
-        workers = args.compile_workers
-    runner = measure.configure(device=local, workers=workers, cache_dir=cache,
-                               lower_workers=args.lower_workers or max(1, min(8, cores // (2 * world))))
-    runner.context(dag, 0)                             # inputs + fp64 ground truth resident
-
-    B = args.batch
-    need = (args.warmup + args.steps) * B * world
-    if need > len(stream):
-        raise SystemExit(f"stream has {len(stream)} States, run needs {need}")
-
-    def batch(step: int):
-        """The whole step's batch (B per rank); each rank measures its own shard."""
-        lo = step * world * B
-        return [replay(dag, h) for h in stream[lo:lo + world * B]]
+    workers = args.compile_workers or max(1, cores // world - (1 if world == 1 else 0))
+    lower_workers = args.lower_workers or max(1, min(8, cores // (2 * world)))
+    runner = measure.configure(device=local, workers=workers, cache_dir=tempfile.mkdtemp(prefix="lt_cubin_"),
+                               lower_workers=lower_workers)
+    l2_flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")     # 256 MB > 126 MB L2
 
     def sync():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
 
-    all_recs = []
-    launch_log = []
-    refresh_s = []
-
-    l2_flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")     # 256 MB > 126 MB L2
-
-    def run_steps(first: int, n: int, fresh_ctx: bool) -> float:
+    def run_steps(dag, stream, first: int, n: int, e2e: bool) -> tuple:
         """Time n steps with CUDA events on the current stream; max over ranks."""
-        progs = [batch(first + s) for s in range(n)]
+        progs = [[replay(dag, h) for h in step_slice(stream, first + s, args.batch, world)] for s in range(n)]
+        results, records = [], []
         sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for ps in progs:
             l2_flush.zero_()                   # 256 MB write: no step starts with a warm L2
-            if fresh_ctx:   # e2e: inputs re-uploaded and ground truth recomputed inside the region
-                t_r = time.perf_counter()
-                for c in runner.ctx.values():
-                    c.refresh()
-                refresh_s.append(time.perf_counter() - t_r)
-            res = sharded_measure(ps)          # NCCL all_gather of (status, cost) records
-            all_recs.append(res)
-            launch_log.append(list(runner.last_records))
+            if e2e:                            # inputs from pinned host memory, ground truth recomputed
+                runner.refresh()
+            results.append(sharded_measure(ps))          # NCCL all_gather of (status, cost) records
+            records.append(list(runner.last_records))
         e1.record()
         sync()
         ms = e0.elapsed_time(e1)
@@ -358,123 +443,181 @@ def main() -> None:
             t = torch.tensor([ms], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms
+        return ms, results, records
 
-    run_steps(0, args.warmup, False)                               # warm-up (NVRTC workers, clocks)
-    runner.stats.update({k: 0 if isinstance(v, int) else 0.0 for k, v in runner.stats.items()})
-    with Clocks(local) as clk:
-        ms = run_steps(args.warmup, args.steps, False)
-    stats = dict(runner.stats)
-    timed = all_recs[-args.steps:]
+    def summarise(cfg, ms, results, records, steps) -> dict:
+        n_total = sum(len(rs) for rs in results)
+        costs = [r.cost for rs in results for r in rs if r.status == "valid"]
+        best_us = min(costs) if costs else float("nan")
+        best = min((r for rs in records for r in rs if r.status == "valid"), key=lambda r: r.cost_us, default=None)
+        achieved = FLOPS[cfg] / (best_us * 1e-6) / 1e12 if math.isfinite(best_us) else None
+        return {"value": n_total / (ms / 1000.0), "ms": ms, "ms_per_step": ms / steps, "measured": n_total,
+                "valid": len(costs), "best_us": best_us, "achieved": achieved,
+                "best_sha1": best.key if best else None, "best_kernels": best.info.get("kernels") if best else None}
+
+    # ---- headline config --------------------------------------------------------------
+    dag, stream = load_stream(args.config)
+    need = (args.warmup + args.steps) * args.batch * world
+    if need > len(stream):
+        raise SystemExit(f"stream has {len(stream)} States, run needs {need}")
+    runner.prepare(dag, 0)                                   # inputs + fp64 ground truth resident
+    run_steps(dag, stream, 0, args.warmup, False)           # warm-up: compile workers, clocks, lowering pool
+    for k in list(runner.stats):
+        runner.stats[k] = 0 if isinstance(runner.stats[k], int) else 0.0
     io0 = dict(runner.io)
-    timed_records = [r for step in launch_log[-args.steps:] for r in step]
+    with Clocks(local) as clk:
+        ms, results, records = run_steps(dag, stream, args.warmup, args.steps, False)
+    stats = dict(runner.stats)
+    head = summarise(args.config, ms, results, records, args.steps)
+    timed_records = [r for step in records for r in step]
     # our kernels launched in the timed region: per measured candidate, its kernels x
-    # (warm-up + repeats), plus one NaN-poison and one verification launch per output
+    # (warm-up + repeats), one NaN-poison and one verification launch per output, one
+    # poison launch per intermediate buffer
     n_launch = sum(len(r.info.get("kernels", [])) * (1 + r.repeats) + 2 * r.n_outputs
                    for r in timed_records if r.n_outputs)
     io1 = dict(runner.io)
-    # e2e re-measures the timed steps' own States from scratch (modules dropped,
-    # compile pool restarted on an empty cubin cache), so value and e2e differ only
-    # by the end-to-end work
-    runner.forget_compiled(tempfile.mkdtemp(prefix="lt_cubin_e2e_"))
-    e2e_ms = run_steps(args.warmup, args.steps, True)
-    io2 = dict(runner.io)
-    h2d_step = (io2["h2d"] - io1["h2d"]) / args.steps
-    d2h_step = (io2["d2h"] - io1["d2h"]) / args.steps
 
-    # every rank already holds the gathered, input-ordered results of each step
-    n_total = sum(len(rs) for rs in timed)
-    n_valid = sum(r.status == "valid" for rs in timed for r in rs)
-    costs = [r.cost for rs in timed for r in rs if r.status == "valid"]
-    best_us = min(costs) if costs else float("nan")
-    best_rec = min((r for r in timed_records if r.status == "valid"), key=lambda r: r.cost_us, default=None)
-    value = n_total / (ms / 1000.0)
-    e2e = (args.steps * B * world) / (e2e_ms / 1000.0)
-    if world > 1:   # launches of all ranks
+    # e2e: the timed steps' own States from scratch through the public API
+    runner.close()
+    runner = measure.configure(device=local, workers=workers, cache_dir=tempfile.mkdtemp(prefix="lt_cubin_e2e_"),
+                               lower_workers=lower_workers)
+    runner.prepare(dag, 0)
+    io_e0 = dict(runner.io)
+    e2e_ms, _, _ = run_steps(dag, stream, args.warmup, args.steps, True)
+    io_e1 = dict(runner.io)
+    h2d_step = (io_e1["h2d"] - io_e0["h2d"]) / args.steps
+    d2h_step = (io_e1["d2h"] - io_e0["d2h"]) / args.steps
+    e2e = args.steps * args.batch * world / (e2e_ms / 1000.0)
+
+    # ---- sub-configs (north_star's named operators) ----------------------------------------
+    subs = {}
+    for cfg in [c for c in args.sub_configs.split(",") if c and c != args.config]:
+        sdag, sstream = load_stream(cfg)
+        runner.prepare(sdag, 0)
+        run_steps(sdag, sstream, 0, 1, False)
+        sms, sres, srec = run_steps(sdag, sstream, 1, args.sub_steps, False)
+        subs[cfg] = summarise(cfg, sms, sres, srec, args.sub_steps)
+        subs[cfg]["stream_states"] = [args.batch * world, (1 + args.sub_steps) * args.batch * world]
+
+    if world > 1:
         t = torch.tensor([n_launch], device="cuda")
         dist.all_reduce(t)
         n_launch = int(t.item())
 
     if rank == 0:
-        lib = rt.load()
         import ctypes
+        lib = rt.load()
         tf, pms = ctypes.c_double(), ctypes.c_double()
         rt.check(lib.lt_ffma_peak(local, ctypes.byref(tf), ctypes.byref(pms)), "ffma peak")
         peak = tf.value
-        achieved = FLOPS[args.config] / (best_us * 1e-6) / 1e12 if math.isfinite(best_us) else None
         peaks = {}
         try:
             peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         except (OSError, ValueError):
             pass
+
+        def roofline(s):
+            return {"bound": "fp32", "achieved": s["achieved"], "peak": peak, "unit": "TFLOP/s",
+                    "frac": (s["achieved"] / peak) if s["achieved"] else None, "traffic": traffic_of(s["best_sha1"] or ""),
+                    "kernel": "best candidate of the timed steps (cost = mean of CUDA-event repeats on the "
+                              "candidate's stream)",
+                    "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU (148 SM x 128 lanes "
+                                   "x 2 x clock)"}
+
         line = {
-            "metric": f"measured candidates/sec ({args.config}, SSSRRSRS, compile+run+verify)",
-            "value": value, "unit": "cand/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
-            "config": {"workload": NAMES[args.config], "candidates_per_rank_per_step": B,
+            "metric": metric(args.config), "value": head["value"], "unit": "cand/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": NAMES[args.config], "candidates_per_rank_per_step": args.batch,
                        "stream": f"tests/golden/streams/{args.config}.json.gz (reference sampler, legal launches)",
-                       "compile_workers_per_rank": workers, "cubin_cache": "empty at start",
-                       "l2": "flushed before every timed step (256 MB write); a candidate's cost is the "
-                             "mean of back-to-back repeats after its warm-up run (TVM time_evaluator semantics)"},
-            "valid": n_valid, "measured": n_total,
-            "best_program": {"us": best_us, "tflops": achieved, "flop": FLOPS[args.config],
-                             "source_sha1": best_rec.key if best_rec else None,
-                             "kernels": (best_rec.info.get("kernels") if best_rec else None)},
+                       "timed_states": [args.warmup * args.batch * world, need],
+                       "compile_workers_per_rank": workers, "cubin_cache": "empty at start", "rate": RATE_DEF,
+                       "l2": "flushed before every timed step (256 MB write); a candidate's cost is the mean of "
+                             "back-to-back repeats after its verified warm-up run"},
+            "valid": head["valid"], "measured": head["measured"],
+            "best_program": {"us": head["best_us"], "tflops": head["achieved"], "flop": FLOPS[args.config],
+                             "source_sha1": head["best_sha1"], "kernels": head["best_kernels"]},
             "compile": {"compiled": stats["compiled"], "cache_hits": stats["cache_hits"],
                         "recompiled_O1": stats.get("recompiled", 0),
                         "kernels_compiled": stats.get("kernels_compiled", 0),
                         "kernels_shared": stats.get("kernels_shared", 0),
                         "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
             "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s")},
-            "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None,
-                         "traffic": traffic_of(best_rec.key if best_rec else ""),
-                         "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the best "
-                                         "candidate (ncu --set full, profiles/traffic.json by source sha1; "
-                                         "null when this run's best was not profiled)",
-                         "kernel": "best candidate of the timed steps (cost = mean of CUDA-event repeats)",
-                         "peak_source": "lt_ffma_peak: FFMA issue-bound microbenchmark on this GPU"},
+            "roofline": roofline(head),
             "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
-                    "d2h_bytes_per_step": int(d2h_step),
-                    "refresh_ms_per_step": 1e3 * sum(refresh_s) / max(1, len(refresh_s)),
-                    "ms_per_step": e2e_ms / args.steps,
-                    "note": "measure_batch on host Programs; every step re-uploads the DAG's input tensors "
-                            "(fp32+fp64, pageable) and recomputes the fp64 ground truth on the device; cubins "
-                            "H2D; per-candidate error words D2H"},
+                    "d2h_bytes_per_step": int(d2h_step), "ms_per_step": e2e_ms / args.steps,
+                    "note": "measure_batch from a fresh measuring process (new CUDA context, empty cubin cache); "
+                            "every step re-uploads the DAG's inputs (fp32 + fp64) and recomputes the fp64 ground "
+                            "truth; cubins and launch lists H2D; per-candidate error words D2H"},
             "gpu_launches": n_launch,
+            "clocks": clk.summary(),
+            "faults": {"device_faults": stats.get("device_faults", 0), "restarts": stats.get("restarts", 0)},
         }
-        line["clocks"] = clk.summary()
+        line["configs"] = {c: {"metric": metric(c), "value": s["value"], "unit": "cand/s",
+                               "steps": args.sub_steps, "measured": s["measured"], "valid": s["valid"],
+                               "best_program": {"us": s["best_us"], "tflops": s["achieved"], "flop": FLOPS[c],
+                                                "source_sha1": s["best_sha1"]},
+                               "roofline": roofline(s), "timed_states": s["stream_states"]}
+                           for c, s in subs.items()}
         if not args.no_scoring:
-            line["train"] = train_bench()
             progs = [replay(dag, h) for h in stream[:256]]
             sb = scoring_bench(local, progs)
             rows_bytes = sb["n_stmt"] * 164 * 8
             fbytes = sb["words_bytes"] + rows_bytes
+            tbytes = sb["n_stmt"] * sb["n_used"] * 8 + sb["n_stmt"] * 8
             hbm = peaks.get("hbm_gbs")
+
+            def hbm_roof(nbytes, ms, what):
+                ach = nbytes / (ms / 1000) / 1e9
+                return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                        "frac": ach / hbm if hbm else None, "traffic": None, "algorithmic_bytes": nbytes,
+                        "bytes_def": what, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
             line["scoring"] = {
                 "programs": sb["n_prog"], "statements": sb["n_stmt"],
-                "device_programs_per_s": sb["n_prog"] / ((sb["features_ms"] + sb["trees_ms"]) / 1000),
+                "device_programs_per_s": sb["n_prog"] / ((sb["features_ms"] + sb["trees_ms"] + sb["segsum_ms"]) / 1000),
                 "e2e_programs_per_s": sb["n_prog"] / sb["e2e_s"],
-                "features_ms": sb["features_ms"], "trees_ms": sb["trees_ms"],
-                "roofline_features": {"bound": "hbm", "achieved": fbytes / (sb["features_ms"] / 1000) / 1e9,
-                                      "peak": hbm, "unit": "GB/s",
-                                      "frac": (fbytes / (sb["features_ms"] / 1000) / 1e9) / hbm if hbm else None,
-                                      "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}}
-        # CPU baseline: the reference's runner restated, bounded sample, all host cores
-        cb = cpu_reference(stream[-cores:], dag, args.cpu_seconds, cores)
-        cf = cpu_reference(stream[-cores:], dag, args.cpu_seconds, cores, fn=_cpu_full)
-        line["cpu_full_execution"] = {
-            "value": cf["value"], "unit": "cand/s", "cores": cores, "kind": "port",
-            "sample": f"{cf['candidates']} stream States (one per core): full-size `interpret` "
-                      f"(oracle/interp.py), {cf['truncated']} capped at {args.cpu_seconds:g} s and counted with "
-                      "that time (an upper bound on the reference's rate of really executing candidates)"}
-        line["cpu_baseline"] = {"value": cb["value"], "unit": "cand/s", "cores": cores, "kind": "port",
-                                "sample": f"{cb['candidates']} stream States (one per core) through "
-                                          "oracle/machine.py measure_batch (validate + twin interpret + "
-                                          f"machine_cost); {cb['truncated']} capped at {args.cpu_seconds:g} s "
-                                          "and counted with that time (optimistic)"}
+                "features_ms": sb["features_ms"], "trees_ms": sb["trees_ms"], "segsum_ms": sb["segsum_ms"],
+                "roofline_features": hbm_roof(fbytes, sb["features_ms"], "encoded words read + rows x 164 x 8 B written"),
+                "roofline_trees": hbm_roof(tbytes, sb["trees_ms"],
+                                           f"rows x {sb['n_used']} used feature columns x 8 B read + rows x 8 B "
+                                           "written (the model is shared-memory resident)")}
+            line["train"] = train_bench()
+        if not args.no_cpu:
+            pool = RefPool(cores)
+            try:
+                timed_h = [h for s in range(args.warmup, args.warmup + args.steps)
+                           for h in step_slice(stream, s, args.batch, world)]
+                sample = timed_h[:cores]
+                cb = ref_measure_rate(pool, dag, sample, args.cpu_seconds)
+                line["cpu_baseline"] = {
+                    "value": cb["value"], "unit": "cand/s", "cores": cores, "kind": "reference",
+                    "sample": f"the first {cb['candidates']} timed States through loomtune.machine.measure_batch, "
+                              f"one per process; {cb['capped']} stopped at the {args.cpu_seconds:g} s cap and "
+                              "counted as measured (optimistic)"}
+                cf = ref_interpret_rate(pool, dag, sample, args.cpu_seconds)
+                line["cpu_full_execution"] = {
+                    "value": cf["value"], "unit": "cand/s", "cores": cores, "kind": "reference",
+                    "sample": f"the same {cf['candidates']} States: full-size loomtune.interp.interpret (the "
+                              f"reference's only real execution of a State); {cf['capped']} stopped at the "
+                              f"{args.cpu_seconds:g} s cap and counted as done (an upper bound)"}
+                model_json = json.load(open(os.path.join(ROOT, "tests", "golden", "model.json")))
+                cp = ref_predict_rate(pool, dag, stream[:256] * max(1, 2 * cores // 16), model_json)
+                line["cpu_predict"] = {
+                    "value": cp["value"], "unit": "programs/s", "cores": cores, "kind": "reference",
+                    "sample": f"{cp['programs']} stream programs through loomtune extract_features + "
+                              "CostModel.predict (tests/golden/model.json, 30 trees), chunks of 16 per process"}
+                for c in subs:
+                    sdag, sstream = load_stream(c)
+                    r = ref_measure_rate(pool, sdag, step_slice(sstream, 1, args.batch, world)[:cores],
+                                         args.cpu_seconds)
+                    line["configs"][c]["cpu_baseline"] = {
+                        "value": r["value"], "unit": "cand/s", "cores": cores, "kind": "reference",
+                        "sample": f"the first {r['candidates']} timed States through loomtune.machine.measure_batch; "
+                                  f"{r['capped']} capped at {args.cpu_seconds:g} s"}
+            finally:
+                pool.close()
         print(json.dumps(line))
+    runner.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

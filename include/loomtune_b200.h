@@ -29,21 +29,14 @@ int lt_version(void);
 int lt_device_count(void);
 int lt_set_device(int device);
 void lt_release_scratch(void);
-/* Setup: checks that n_gpus devices are visible, creates each
- * device's runner context and starts the compile pool (n_workers <= 0: host
- * cores - 1) with an on-disk cubin cache in cache_dir (NULL/"": none). */
+/* Setup: checks that n_gpus devices are visible, creates
+ * their contexts and starts the compile pool (n_workers <= 0: host cores - 1)
+ * with an on-disk cubin cache in cache_dir (NULL/"": none). */
 int lt_init(int n_gpus, const char* cache_dir, int n_workers);
-/* Teardown before process exit: compile pool stopped (workers reaped), runner
- * contexts destroyed, scratch freed.  Model/training handles stay valid until
- * their destroy calls. */
+/* Teardown before process exit: compile pool stopped (workers reaped), scratch
+ * freed.  Task, module, model and training handles stay valid until their
+ * destroy calls. */
 int lt_shutdown(void);
-/* Candidate kernels run in a private per-device "runner" context, never in the
- * primary context (torch, NCCL, scoring and training kernels).  After a kernel
- * fault (lt_measure_record.status == 2) lt_runner_reset destroys that context:
- * every task and candidate module of `device` created before becomes invalid;
- * nothing else is touched.  lt_runner_generation counts the resets. */
-int lt_runner_reset(int device);
-int lt_runner_generation(int device);
 
 /* ---- (B) feature extraction --------------------------------------------
  * Replaces extract_features / analyze_program / statement_features
@@ -128,7 +121,8 @@ typedef struct {
   double first_us;      /* warm-up run */
   float max_rel_err;    /* worst relative error over checked outputs (inf if NaN) */
   int32_t repeats;
-  int32_t status;       /* 0 ok, 1 launch refused (resources), 2 kernel fault (reset the runner context) */
+  int32_t status;       /* 0 ok, 1 launch refused (resources), 2 kernel fault: the process's CUDA
+                           state is lost (every context on the device), restart the process */
   char detail[200];
 } lt_measure_record;
 
@@ -138,7 +132,6 @@ int64_t lt_module_function(int64_t module, const char* name);
 int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads, int* static_smem);
 int64_t lt_task_create(int device);
 void lt_task_destroy(int64_t task);
-void lt_task_abandon(int64_t task);      /* host record only, after lt_runner_reset */
 void* lt_task_stream(int64_t task);
 int lt_task_slot(int64_t task, int slot, int64_t bytes);
 int64_t lt_task_slot_ptr(int64_t task, int slot);

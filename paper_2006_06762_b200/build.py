@@ -64,7 +64,7 @@ def build(verbose: bool = False) -> str:
                 print(" ".join(cmd))
             _run(cmd)
     if _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", os.path.join(CUDA, "lib64"), "-lcudart",
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", os.path.join(CUDA, "lib64"), "-lcudart", "-ldl",
               "-Xlinker", "-rpath=" + os.path.join(CUDA, "lib64")])
     wsrc = os.path.join(CSRC, "nvrtc_worker.cpp")
     if os.path.exists(wsrc) and _stale(WORKER, [wsrc] + headers):

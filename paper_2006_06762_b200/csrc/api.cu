@@ -17,8 +17,6 @@ extern "C" int lt_cols_to_rows_device(const double*, int64_t, double*, void*);
 extern "C" int lt_predict_rows_device(int64_t, const double*, int64_t, double*, void*);
 extern "C" int lt_predict_cols_device(int64_t, const double*, int64_t, double*, void*);
 extern "C" int lt_segment_sum_device(const double*, const int64_t*, int64_t, double*, void*);
-extern "C" int lt_runner_reset(int);
-extern "C" int lt_runner_generation(int);
 extern "C" int lt_pool_start(int, const char*, double);
 extern "C" void lt_pool_stop(void);
 
@@ -150,7 +148,7 @@ int lt_score_batch(int64_t model, const int32_t* words, const int64_t* stmt_off,
   return lt::check_cuda(cudaStreamSynchronize(s.stream), "score copy-back");
 }
 
-// Library setup: check the devices, create each device's runner context and
+// Library setup: check the devices, create each device's primary context and
 // start the compile pool (n_workers <= 0: host cores - 1) on `cache_dir`
 // (NULL or "": no on-disk cubin cache).
 int lt_init(int n_gpus, const char* cache_dir, int n_workers) {
@@ -158,7 +156,8 @@ int lt_init(int n_gpus, const char* cache_dir, int n_workers) {
   if (n_gpus < 1 || n_gpus > n) return lt::fail("lt_init: " + std::to_string(n_gpus) + " GPUs asked, " +
                                                 std::to_string(n) + " visible");
   for (int d = 0; d < n_gpus; ++d)
-    if (lt_runner_generation(d) < 0) return lt::fail("lt_init: bad device");
+    if (lt::check_cuda(cudaSetDevice(d), "lt_init: cudaSetDevice") || lt::check_cuda(cudaFree(0), "lt_init: context"))
+      return -1;
   if (n_workers <= 0) {
     long c = sysconf(_SC_NPROCESSORS_ONLN);
     n_workers = c > 1 ? (int)c - 1 : 1;
@@ -167,13 +166,10 @@ int lt_init(int n_gpus, const char* cache_dir, int n_workers) {
 }
 
 // Library teardown, before process exit: stop the compile pool (joins its
-// dispatcher thread and reaps the workers), destroy every runner context (task
-// buffers and candidate modules go with them) and free the scoring scratch.
-// Model and training handles stay valid until their destroy calls.
+// dispatcher thread and reaps the workers) and free the scoring scratch.  Task,
+// module, model and training handles stay valid until their destroy calls.
 int lt_shutdown(void) {
   lt_pool_stop();
-  int n = lt_device_count();
-  for (int d = 0; d < n; ++d) lt_runner_reset(d);
   std::lock_guard<std::mutex> g(lt::g_mu);
   lt::g_s.release();
   return 0;

@@ -39,11 +39,6 @@ struct Drv {
   CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                            CUstream, void**, void**) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
-  CUresult (*DeviceGet)(CUdevice*, int) = nullptr;
-  CUresult (*CtxCreate)(CUcontext*, unsigned, CUdevice) = nullptr;
-  CUresult (*CtxDestroy)(CUcontext) = nullptr;
-  CUresult (*CtxPushCurrent)(CUcontext) = nullptr;
-  CUresult (*CtxPopCurrent)(CUcontext*) = nullptr;
   bool ok = false;
 };
 static Drv g_drv;
@@ -53,7 +48,7 @@ template <class F>
 static bool resolve(const char* name, F& fn) {
   cudaDriverEntryPointQueryResult q;
   void* p = nullptr;
-  if (cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
   fn = reinterpret_cast<F>(p);
   return true;
 }
@@ -65,10 +60,7 @@ static const Drv* drv() {
               resolve("cuModuleGetFunction", g_drv.ModuleGetFunction) &&
               resolve("cuFuncGetAttribute", g_drv.FuncGetAttribute) &&
               resolve("cuFuncSetAttribute", g_drv.FuncSetAttribute) &&
-              resolve("cuLaunchKernel", g_drv.LaunchKernel) && resolve("cuGetErrorString", g_drv.GetErrorString) &&
-              resolve("cuDeviceGet", g_drv.DeviceGet) && resolve("cuCtxCreate", g_drv.CtxCreate) &&
-              resolve("cuCtxDestroy", g_drv.CtxDestroy) && resolve("cuCtxPushCurrent", g_drv.CtxPushCurrent) &&
-              resolve("cuCtxPopCurrent", g_drv.CtxPopCurrent);
+              resolve("cuLaunchKernel", g_drv.LaunchKernel) && resolve("cuGetErrorString", g_drv.GetErrorString);
     if (!ok) {
       fail("CUDA driver entry points unavailable (no driver / no device)");
       return nullptr;
@@ -89,56 +81,17 @@ static int check_cu(CUresult r, const char* what) {
   return fail(std::string(what) + ": " + cu_str(r));
 }
 
-// ---- the runner's private context ------------------------------------------
-// Candidate kernels run in a context of their own (cuCtxCreate), never in the
-// device's primary context that torch, NCCL and this library's scoring/training
-// kernels share.  A faulting candidate leaves a sticky error in that context
-// only: lt_runner_reset() destroys it (freeing every task buffer and candidate
-// module with it) and the next runner call creates a fresh one; the primary
-// context and everything allocated in it are untouched.
-static const int kMaxDev = 64;
-static CUcontext g_ctx[kMaxDev];
-static int g_ctx_gen[kMaxDev];     // incremented per reset: handles of older generations are dead
-static std::mutex g_ctx_mu;
-static std::unordered_map<CUmodule, std::pair<int, int>> g_mod;   // module -> (device, generation)
-
-static CUcontext runner_ctx(int device) {
-  if (device < 0 || device >= kMaxDev) { fail("device index out of range"); return nullptr; }
-  const Drv* d = drv();
-  if (!d) return nullptr;
-  std::lock_guard<std::mutex> g(g_ctx_mu);
-  if (!g_ctx[device]) {
-    CUdevice dev;
-    CUcontext c = nullptr;
-    if (check_cu(d->DeviceGet(&dev, device), "cuDeviceGet") ||
-        check_cu(d->CtxCreate(&c, CU_CTX_SCHED_AUTO, dev), "cuCtxCreate"))
-      return nullptr;
-    CUcontext top;
-    d->CtxPopCurrent(&top);           // cuCtxCreate made it current: callers push it per call
-    g_ctx[device] = c;
-  }
-  return g_ctx[device];
-}
-
-// Makes the runner context current for the scope of one C-ABI call (runtime-API
-// calls inside — cudaMalloc, streams, events, <<<>>> launches — use it).
-struct CtxScope {
-  bool ok = false;
-  explicit CtxScope(int device) {
-    CUcontext c = runner_ctx(device);
-    ok = c && !check_cu(g_drv.CtxPushCurrent(c), "cuCtxPushCurrent");
-  }
-  ~CtxScope() {
-    if (ok) {
-      CUcontext top;
-      g_drv.CtxPopCurrent(&top);
-    }
-  }
-};
+// A faulting candidate (illegal address, ...) leaves a sticky error that kills
+// every CUDA context of the process on that device (measured on the B200: the
+// primary context and a fresh cuCtxCreate both fail afterwards).  Faults are
+// therefore contained by a process boundary: lt_measure reports status 2 and
+// the caller restarts its measuring process (the Python runner measures in a
+// child process, paper_2006_06762_b200/measure.py).
+static std::mutex g_mod_mu;
+static std::unordered_map<CUmodule, int> g_mod;   // module -> device
 
 struct Task {
   int device = 0;
-  int gen = 0;                     // runner-context generation the task lives in
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::unordered_map<int, std::pair<void*, int64_t>> slots;
@@ -207,30 +160,30 @@ typedef struct {
 
 int64_t lt_module_load(int device, const void* image, int64_t len) {
   (void)len;
-  lt::CtxScope cs(device);
-  if (!cs.ok) return 0;
+  if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return 0;
+  cudaFree(0);  // make the primary context current for the driver API
+  const lt::Drv* d = lt::drv();
+  if (!d) return 0;
   CUmodule m;
-  if (lt::check_cu(lt::g_drv.ModuleLoadData(&m, image), "cuModuleLoadData")) return 0;
-  std::lock_guard<std::mutex> g(lt::g_ctx_mu);
-  lt::g_mod[m] = {device, lt::g_ctx_gen[device]};
+  if (lt::check_cu(d->ModuleLoadData(&m, image), "cuModuleLoadData")) return 0;
+  std::lock_guard<std::mutex> g(lt::g_mod_mu);
+  lt::g_mod[m] = device;
   return (int64_t)(intptr_t)m;
 }
 
 int lt_module_unload(int64_t module) {
   CUmodule m = (CUmodule)(intptr_t)module;
-  int device, gen;
+  int device;
   {
-    std::lock_guard<std::mutex> g(lt::g_ctx_mu);
+    std::lock_guard<std::mutex> g(lt::g_mod_mu);
     auto it = lt::g_mod.find(m);
     if (it == lt::g_mod.end()) return lt::fail("cuModuleUnload: unknown module");
-    device = it->second.first;
-    gen = it->second.second;
+    device = it->second;
     lt::g_mod.erase(it);
-    if (gen != lt::g_ctx_gen[device]) return 0;     // freed with its reset context
   }
-  lt::CtxScope cs(device);
-  if (!cs.ok) return -1;
-  return lt::check_cu(lt::g_drv.ModuleUnload(m), "cuModuleUnload");
+  const lt::Drv* d = lt::drv();
+  if (!d || lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return -1;
+  return lt::check_cu(d->ModuleUnload(m), "cuModuleUnload");
 }
 
 int64_t lt_module_function(int64_t module, const char* name) {
@@ -260,38 +213,10 @@ int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads
   return 0;
 }
 
-// Destroy the runner context of `device` after a kernel fault (or to start from
-// scratch): every task buffer and candidate module in it is freed with it.  The
-// primary context (torch tensors, NCCL, scoring and training state) is untouched.
-int lt_runner_reset(int device) {
-  if (device < 0 || device >= lt::kMaxDev) return lt::fail("device index out of range");
-  const lt::Drv* d = lt::drv();
-  if (!d) return -1;
-  CUresult r = CUDA_SUCCESS;
-  {
-    std::lock_guard<std::mutex> g(lt::g_ctx_mu);
-    if (lt::g_ctx[device]) r = d->CtxDestroy(lt::g_ctx[device]);
-    lt::g_ctx[device] = nullptr;
-    ++lt::g_ctx_gen[device];
-  }
-  lt::runner_forget();
-  return lt::check_cu(r, "cuCtxDestroy");
-}
-
-// Number of runner-context resets of `device` so far (tasks and modules created
-// before the last one are dead).
-int lt_runner_generation(int device) {
-  if (device < 0 || device >= lt::kMaxDev) return -1;
-  std::lock_guard<std::mutex> g(lt::g_ctx_mu);
-  return lt::g_ctx_gen[device];
-}
-
 int64_t lt_task_create(int device) {
-  lt::CtxScope cs(device);
-  if (!cs.ok) return 0;
+  if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return 0;
   Task* t = new Task();
   t->device = device;
-  t->gen = lt_runner_generation(device);
   if (lt::check_cuda(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream") ||
       lt::check_cuda(cudaEventCreate(&t->ev0), "event") || lt::check_cuda(cudaEventCreate(&t->ev1), "event") ||
       lt::check_cuda(cudaMalloc(&t->d_err, 16), "cudaMalloc")) {
@@ -301,34 +226,23 @@ int64_t lt_task_create(int device) {
   return (int64_t)(intptr_t)t;
 }
 
-// Free the host-side task record only (its device objects died with a reset).
-void lt_task_abandon(int64_t handle) { delete (Task*)(intptr_t)handle; }
-
-static bool task_live(const Task* t) { return t->gen == lt_runner_generation(t->device); }
-
 void lt_task_destroy(int64_t handle) {
   Task* t = (Task*)(intptr_t)handle;
   if (!t) return;
-  if (task_live(t)) {
-    lt::CtxScope cs(t->device);
-    if (cs.ok) {
-      cudaStreamSynchronize(t->stream);
-      for (auto& kv : t->slots) cudaFree(kv.second.first);
-      cudaFree(t->d_err);
-      cudaEventDestroy(t->ev0);
-      cudaEventDestroy(t->ev1);
-      cudaStreamDestroy(t->stream);
-    }
-  }
+  cudaSetDevice(t->device);
+  cudaStreamSynchronize(t->stream);
+  for (auto& kv : t->slots) cudaFree(kv.second.first);
+  cudaFree(t->d_err);
+  cudaEventDestroy(t->ev0);
+  cudaEventDestroy(t->ev1);
+  cudaStreamDestroy(t->stream);
   delete t;
 }
 
 void* lt_task_stream(int64_t handle) { return ((Task*)(intptr_t)handle)->stream; }
 
-#define TASK_SCOPE(t)                                                                      \
-  if (!task_live(t)) return lt::fail("task belongs to a runner context that was reset"); \
-  lt::CtxScope cs_((t)->device);                                                           \
-  if (!cs_.ok) return -1
+#define TASK_SCOPE(t) \
+  if (lt::check_cuda(cudaSetDevice((t)->device), "cudaSetDevice")) return -1
 
 static int slot_alloc(Task* t, int slot, int64_t bytes) {
   auto it = t->slots.find(slot);
@@ -391,7 +305,8 @@ int lt_task_fill(int64_t handle, int slot, int64_t n, uint32_t value) {
 }
 
 static int launch_list(Task* t, const lt_launch* ls, int n, std::string& why) {
-  const lt::Drv* d = &lt::g_drv;
+  const lt::Drv* d = lt::drv();
+  if (!d) { why = "CUDA driver unavailable"; return 2; }
   for (int i = 0; i < n; ++i) {
     const lt_launch& L = ls[i];
     CUfunction f = (CUfunction)(intptr_t)L.func;
@@ -434,9 +349,9 @@ int lt_task_run(int64_t handle, const lt_launch* launches, int n) {
   return lt::check_cuda(cudaStreamSynchronize(t->stream), "run");
 }
 
-// A sticky error after launching: the candidate faulted and the runner context
-// is unusable.  Reported as status 2 (the caller resets the runner context);
-// never an error return, so measure_batch keeps its never-raises contract.
+// A sticky error after launching: the candidate faulted and the process's CUDA
+// state is lost.  Reported as status 2 (the caller restarts the measuring
+// process); never an error return, so measure_batch keeps its never-raises contract.
 static int faulted(lt_measure_record* rec, const char* where, cudaError_t e) {
   rec->status = 2;
   snprintf(rec->detail, sizeof rec->detail, "kernel fault (%s): %s", where, cudaGetErrorString(e));

@@ -91,6 +91,7 @@ class Record:
     n_outputs: int = 0
     info: dict = field(default_factory=dict)
     key: str = ""             # sha1 of the candidate's generated source
+    done: bool = False        # final (False: not reached before a fault ended the batch)
 
 
 def random_inputs(dag, seed: int) -> dict:
@@ -274,8 +275,9 @@ def _lower_one(p, backend: str):
     return "ok", lo, time.perf_counter() - t0
 
 
-class Runner:
-    """Per-process GPU runner: one device, one compile pool, DAG contexts, module cache.
+class RunnerCore:
+    """The GPU runner proper (lives in the measuring process, see `Runner`): one
+    device, one compile pool, DAG contexts, module cache.
 
     Host work per candidate (validate + lowering, pure Python) runs in a pool of
     lowering processes so it neither serialises the batch nor holds the GIL the
@@ -312,6 +314,7 @@ class Runner:
         self.lower_workers = (lower_workers if lower_workers is not None
                               else int(os.environ.get("LT_LOWER_WORKERS", max(1, min(8, (os.cpu_count() or 2) // 2)))))
         self._lpool = None
+        self.faulted = False            # a candidate faulted: this process's CUDA state is lost
 
     def _lower_pool(self):
         main = sys.modules.get("__main__")
@@ -324,21 +327,6 @@ class Runner:
             self._lpool = ProcessPoolExecutor(self.lower_workers, mp_context=mp.get_context("spawn"))
         return self._lpool
 
-    def reset_device(self) -> None:
-        """After a kernel fault (the runner context is unusable): destroy the
-        runner's private context (lt_runner_reset; torch's primary context and
-        the scoring/training state are untouched), drop every module and DAG
-        context (re-created on demand from kept images) and carry on."""
-        rt.runner_reset(self.device)
-        with self.mod_lock:
-            self.modules.clear()
-            self.pinned.clear()
-        for c in self.ctx.values():
-            self.lib.lt_task_abandon(c.task)
-        self.ctx.clear()
-        self._dag_keys.clear()
-        self.stats["device_resets"] = self.stats.get("device_resets", 0) + 1
-
     def forget_compiled(self, cache_dir: str) -> None:
         """Drop every compiled module and restart the compile pool on `cache_dir`
         (benchmarks re-measuring the same States from scratch)."""
@@ -350,6 +338,13 @@ class Runner:
         self.cache_dir = cache_dir
         rt.check(self.lib.lt_pool_start(self.workers, cache_dir.encode() if cache_dir else None,
                                         self.compile_timeout), "compile pool")
+
+    def abandon(self):
+        """After a fault: stop the host-side pools (no CUDA calls: the context is dead)."""
+        if self._lpool is not None:
+            self._lpool.shutdown(wait=False, cancel_futures=True)
+            self._lpool = None
+        self.lib.lt_pool_stop()
 
     def close(self):
         if self._lpool is not None:
@@ -463,6 +458,7 @@ class Runner:
                 self.stats["lower_s"] += secs
                 if kind_ != "ok":
                     recs[i].detail = payload
+                    recs[i].done = True
                     continue
                 lo = payload
                 recs[i].info = lo.info
@@ -542,6 +538,12 @@ class Runner:
                         closed = True
                     else:
                         waiting.append(item)
+                if self.faulted:                # the rest of the batch goes to a fresh process
+                    waiting.clear()
+                    if closed:
+                        return
+                    time.sleep(0.0005)
+                    continue
                 idx = next((k for k, x in enumerate(waiting) if self._ready(x)), None)
                 if idx is None:
                     if closed and not waiting:
@@ -560,6 +562,7 @@ class Runner:
     def _measure_one(self, item, recs, seed) -> None:
         i, p, lo, key, parts = item
         rec = recs[i]
+        rec.done = True
         entries = [k.entry for k in lo.kernels]
         funcs, compiled, rec.cache_hit = [], False, True
         for ents, kkey, job in parts:
@@ -593,9 +596,10 @@ class Runner:
         m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
         if m.status == 2:
             # a faulting candidate is INVALID like any other failure (SPEC.md:522:
-            # measure_batch never raises); the runner context is reset and the batch continues
+            # measure_batch never raises); the process's CUDA state is gone, so the
+            # batch stops here and the parent carries on in a fresh measuring process
             rec.detail = "gpu: " + m.detail.decode(errors="replace")
-            self.reset_device()
+            self.faulted = True
             return
         self.stats["gpu_s"] += time.perf_counter() - t0
         self.stats["measured"] += 1
@@ -609,6 +613,9 @@ class Runner:
         if not (rec.max_rel_err <= GPU_TOL) and lo.source.startswith(".version") and m.status == 0:
             o1 = lo.info.get("ptxas_opt") == "-O1"
             m2 = self._remeasure_safe(lo, key, entries, ctx, PTX_OPTS if o1 else PTX_SAFE_OPTS)
+            if self.faulted:
+                rec.detail = "gpu: kernel fault (recompiled after failing verification)"
+                return
             if m2 is not None and m2.status == 0:
                 m = m2
                 rec.first_us, rec.repeats = m.first_us, m.repeats
@@ -634,11 +641,286 @@ class Runner:
         t0 = time.perf_counter()
         m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
         if m.status == 2:
-            self.reset_device()
+            self.faulted = True
             return None
         self.stats["gpu_s"] += time.perf_counter() - t0
         self.io["d2h"] += 4
         return m
+
+
+# ---- the measuring process -------------------------------------------------
+# A faulting candidate kills every CUDA context of its process on the device
+# (measured: torch's primary context and a fresh cuCtxCreate context both fail
+# after one illegal-address fault), so candidates run in a child process that
+# owns the RunnerCore; the parent (torch, NCCL, the scoring/training kernels)
+# never sees a device fault.  A fault ends the child's batch; the parent starts
+# a fresh child and measures the rest of the batch there.
+
+FAULT_PTX = b""".version 8.7
+.target sm_100a
+.address_size 64
+.visible .entry lt_fault()
+{
+  .reg .b64 %rd<2>;
+  .reg .b32 %r<2>;
+  mov.u64 %rd1, 16;
+  mov.u32 %r1, 7;
+  st.global.u32 [%rd1], %r1;
+  ret;
+}
+"""
+
+
+def _delta(after: dict, before: dict) -> dict:
+    return {k: v - before.get(k, 0) for k, v in after.items() if isinstance(v, (int, float))}
+
+
+class _Server:
+    """Commands the parent's `Runner` sends to the measuring process."""
+
+    def __init__(self, kw: dict):
+        self.core = RunnerCore(**kw)
+
+    def measure(self, programs, seed):
+        c = self.core
+        if len(c._dag_keys) > 256:         # every call unpickles fresh DAG objects
+            c._dag_keys.clear()
+        s0, io0 = dict(c.stats), dict(c.io)
+        recs = c.measure_programs(programs, seed)
+        return recs, _delta(c.stats, s0), _delta(c.io, io0)
+
+    def prepare(self, dag, seed):
+        c = self.core
+        io0 = dict(c.io)
+        c.context(dag, seed)
+        return _delta(c.io, io0)
+
+    def refresh(self):
+        c = self.core
+        io0 = dict(c.io)
+        for ctx in c.ctx.values():
+            ctx.refresh()
+        return _delta(c.io, io0)
+
+    def drop_contexts(self):
+        c = self.core
+        for ctx in c.ctx.values():
+            c.lib.lt_task_destroy(ctx.task)
+        c.ctx.clear()
+        c._dag_keys.clear()
+
+    def download(self, dag, seed, name, numel, fp64):
+        return self.core.context(dag, seed).download(name, numel, fp64)
+
+    def forget_compiled(self, cache_dir):
+        self.core.forget_compiled(cache_dir)
+
+    def set_max_modules(self, n):
+        self.core.max_modules = n
+
+    def inject_fault(self):
+        """Test hook: run a kernel that stores to an unmapped address."""
+        c = self.core
+        m = c.lib.lt_module_load(c.device, FAULT_PTX, len(FAULT_PTX))
+        if not m:
+            raise rt.NativeError(c.lib.lt_last_error().decode())
+        fn = c.lib.lt_module_function(m, b"lt_fault")
+        task = c.lib.lt_task_create(c.device)
+        launches = (rt.Launch * 1)()
+        launches[0].func = fn
+        launches[0].grid[:] = (1, 1, 1)
+        launches[0].block[:] = (32, 1, 1)
+        launches[0].n_args = 0
+        rec = rt.MeasureRecord()
+        zi, zl = np.zeros(1, np.int32), np.zeros(1, np.int64)
+        rt.check(c.lib.lt_measure(task, ctypes.addressof(launches), 1, rt.ptr(zi, rt.c_i32p), rt.ptr(zl, rt.c_i64p),
+                                  0, 1, 5, 1.0, ctypes.addressof(rec)), "lt_measure")
+        c.faulted = c.faulted or rec.status == 2
+        return rec.status, rec.detail.decode(errors="replace")
+
+
+def _serve(conn, kw: dict) -> None:
+    """Measuring-process main loop: (command, args) in, (ok, result) out."""
+    import traceback
+    try:
+        srv = _Server(kw)
+    except BaseException as e:         # surfaced in the parent
+        conn.send((False, f"{type(e).__name__}: {e}"))
+        return
+    conn.send((True, os.getpid()))
+    while True:
+        try:
+            cmd, args = conn.recv()
+        except (EOFError, OSError):
+            break
+        if cmd == "close":
+            srv.core.close()
+            conn.send((True, None))
+            break
+        try:
+            res = getattr(srv, cmd)(*args)
+            conn.send((True, (res, srv.core.faulted)))
+        except BaseException:
+            conn.send((False, traceback.format_exc()))
+        if srv.core.faulted:
+            srv.core.abandon()
+            conn.close()
+            os._exit(0)              # the CUDA state is gone: no teardown calls into it
+
+
+class _ChildDied(RuntimeError):
+    pass
+
+
+class Runner:
+    """The process-wide GPU runner as the rest of the package sees it: forwards
+    to a `RunnerCore` in a child measuring process (spawned on first use,
+    replaced after a kernel fault).  Cumulative `stats` / `io` and the last
+    batch's records (`last_records`) are kept here."""
+
+    def __init__(self, device: int = 0, **kw):
+        self.device = device
+        self._kw = dict(device=device, **kw)
+        self.backend = kw.get("backend", "ptx")
+        self.min_ms = kw.get("min_ms", 1.0)
+        self.stats: dict = {"compiled": 0, "recompiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0,
+                            "kernels_compiled": 0, "kernels_shared": 0, "lower_s": 0.0, "gpu_s": 0.0,
+                            "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0, "restarts": 0}
+        self.io = {"h2d": 0, "d2h": 0}
+        self.last_records: list = []
+        self._max_modules = None
+        self._prepared: list = []          # (dag, seed) made resident; re-made after a restart
+        self._proc = None
+        self._conn = None
+        self.pid = None
+        self._start()
+
+    # -- process management ----------------------------------------------------
+    def _start(self) -> None:
+        import multiprocessing as mp
+        ctx = mp.get_context("spawn")
+        parent, child = ctx.Pipe()
+        proc = ctx.Process(target=_serve, args=(child, self._kw), name="lt-measure", daemon=False)
+        proc.start()
+        child.close()
+        try:
+            ok, payload = parent.recv()
+        except EOFError:
+            proc.join(5)
+            raise rt.NativeError(f"measuring process exited at start (code {proc.exitcode})")
+        if not ok:
+            proc.join(5)
+            raise rt.NativeError(f"measuring process failed to start: {payload}")
+        self._proc, self._conn, self.pid = proc, parent, payload
+        if self._max_modules is not None:
+            self._call("set_max_modules", self._max_modules)
+        for dag, seed in self._prepared:
+            self._call("prepare", dag, seed)
+
+    def _reap(self) -> None:
+        if self._conn is not None:
+            self._conn.close()
+        if self._proc is not None:
+            self._proc.join(10)
+            if self._proc.is_alive():
+                self._proc.kill()
+                self._proc.join(5)
+        self._proc = self._conn = None
+
+    def _call(self, cmd: str, *args):
+        if self._proc is None:
+            self._start()
+            self.stats["restarts"] += 1
+        try:
+            self._conn.send((cmd, args))
+            ok, payload = self._conn.recv()
+        except (EOFError, OSError) as e:
+            code = self._proc.exitcode if self._proc is not None else None
+            self._reap()
+            raise _ChildDied(f"measuring process died (exit code {code})") from e
+        if not ok:
+            raise rt.NativeError(f"measuring process: {payload}")
+        res, faulted = payload
+        if faulted:
+            self._reap()                    # it exits by itself; the next call starts a fresh one
+            self.stats["device_faults"] = self.stats.get("device_faults", 0) + 1
+        return res
+
+    def close(self) -> None:
+        if self._proc is not None:
+            try:
+                self._conn.send(("close", ()))
+                self._conn.recv()
+            except (EOFError, OSError):
+                pass
+            self._reap()
+
+    # -- API -------------------------------------------------------------------
+    def measure_programs(self, programs: list, seed: int = 0) -> list:
+        """Records in input order.  Candidates a fault cut off are measured again
+        in a fresh process; if the process dies outright (not a reported fault),
+        the rest is measured one candidate per call so the culprit is isolated."""
+        programs = list(programs)
+        recs: list = [None] * len(programs)
+        todo = list(range(len(programs)))
+        solo = False
+        while todo:
+            chunk = todo[:1] if solo else todo
+            try:
+                got, dstats, dio = self._call("measure", [programs[i] for i in chunk], seed)
+            except _ChildDied as e:
+                if len(chunk) == 1:
+                    recs[chunk[0]] = Record(detail=f"gpu: {e}", done=True)
+                    todo = todo[1:]
+                solo = True
+                continue
+            for k, v in dstats.items():
+                self.stats[k] = self.stats.get(k, 0) + v
+            for k, v in dio.items():
+                self.io[k] = self.io.get(k, 0) + v
+            for i, r in zip(chunk, got):
+                if r.done:
+                    recs[i] = r
+            todo = [i for i in todo if recs[i] is None]
+        self.last_records = recs
+        return recs
+
+    def prepare(self, dag, seed: int = 0) -> None:
+        """Make a DAG's inputs and fp64 ground truth resident (kept across restarts)."""
+        if not any(d is dag and s == seed for d, s in self._prepared):
+            self._prepared.append((dag, seed))
+        dio = self._call("prepare", dag, seed)
+        for k, v in dio.items():
+            self.io[k] += v
+
+    def refresh(self) -> None:
+        """Re-upload every resident DAG's inputs and recompute its ground truth."""
+        for k, v in self._call("refresh").items():
+            self.io[k] += v
+
+    def drop_contexts(self) -> None:
+        self._prepared.clear()
+        self._call("drop_contexts")
+
+    def download(self, dag, seed: int, name: str, numel: int, fp64: bool = False) -> np.ndarray:
+        """A buffer of the last candidate measured on `dag` (fp64: its ground truth)."""
+        return self._call("download", dag, seed, name, numel, fp64)
+
+    def forget_compiled(self, cache_dir: str) -> None:
+        self._kw["cache_dir"] = cache_dir
+        self._call("forget_compiled", cache_dir)
+
+    @property
+    def max_modules(self):
+        return self._max_modules
+
+    @max_modules.setter
+    def max_modules(self, n: int) -> None:
+        self._max_modules = n
+        self._call("set_max_modules", n)
+
+    def inject_fault(self):
+        return self._call("inject_fault")
 
 
 _RUNNER: Runner | None = None

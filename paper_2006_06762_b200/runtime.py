@@ -55,9 +55,6 @@ _SIGS = [
     ("lt_release_scratch", None, []),
     ("lt_init", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
     ("lt_shutdown", ctypes.c_int, []),
-    ("lt_runner_reset", ctypes.c_int, [ctypes.c_int]),
-    ("lt_runner_generation", ctypes.c_int, [ctypes.c_int]),
-    ("lt_task_abandon", None, [ctypes.c_int64]),
     ("lt_task_fill", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32]),
     # GBDT training (csrc/gbdt.cu)
     ("lt_gbdt_create", ctypes.c_int64, [c_f64p, ctypes.c_int64, ctypes.c_int]),
@@ -136,17 +133,9 @@ def ptr(a: np.ndarray, ctype):
     return a.ctypes.data_as(ctype)
 
 
-def runner_reset(device: int) -> None:
-    """Recover from a kernel fault: destroy the runner's private context on
-    `device` (lt_runner_reset).  Candidate modules and task buffers die with it;
-    the primary context (torch tensors, NCCL, models, training matrices) is
-    untouched."""
-    check(load().lt_runner_reset(device), "runner reset")
-
-
 def shutdown() -> None:
     """lt_shutdown before interpreter teardown (atexit): compile pool joined,
-    runner contexts destroyed, scratch freed; later handle destructors are no-ops."""
+    scratch freed; later handle destructors are no-ops."""
     global epoch
     if _lib is not None:
         epoch += 1

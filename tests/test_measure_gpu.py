@@ -52,10 +52,10 @@ def test_ground_truth_matches_reference_outputs(runner):
               "norm2": dict(n=8, m=32), "grouped_conv2d": dict(h=6, w=6, ci=8, co=8)}
     for name, kw in shapes.items():
         dag = build(name, **kw)
-        ctx = runner.context(dag, 0)
+        runner.prepare(dag, 0)
         for o in dag.outputs:
             want = outs[f"{name}/{o}"]
-            got = ctx.download(o, want.size, fp64=True).reshape(want.shape)
+            got = runner.download(dag, 0, o, want.size, fp64=True).reshape(want.shape)
             np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
 
 
@@ -72,10 +72,9 @@ def test_candidate_outputs_match_reference_outputs(corpus, runner):
         (rec,) = runner.measure_programs([p])
         if rec.status != VALID:
             continue
-        ctx = runner.context(p.dag, 0)
         for o in p.dag.outputs:
             want = outs[f"{name}/{o}"]
-            got = ctx.download(o, want.size).reshape(want.shape).astype(np.float64)
+            got = runner.download(p.dag, 0, o, want.size).reshape(want.shape).astype(np.float64)
             rel = np.abs(got - want) / np.maximum(np.abs(want), 1e-30)
             assert float(rel.max()) <= 1e-4, (i, float(rel.max()))
         checked += 1
@@ -126,32 +125,14 @@ def test_baseline_configs_measure(corpus, runner):
             print("  ", corpus.entries[idx[k]]["dag"], f"{r.cost_us:.1f} us", r.info["kernels"][0].get("template"))
 
 
-FAULT_PTX = b""".version 8.7
-.target sm_100a
-.address_size 64
-.visible .entry lt_fault()
-{
-  .reg .b64 %rd<2>;
-  .reg .b32 %r<2>;
-  mov.u64 %rd1, 16;
-  mov.u32 %r1, 7;
-  st.global.u32 [%rd1], %r1;
-  ret;
-}
-"""
-
-
-def test_kernel_fault_is_contained_in_the_runner_context():
-    """A faulting candidate (illegal address) poisons only the runner's private
-    context: lt_measure reports status 2 (INVALID), lt_runner_reset destroys that
-    context, torch tensors and the cost model's device state in the primary
-    context stay valid, and measurement carries on (modules reload from kept
-    images, DAG contexts are re-created)."""
-    import ctypes
+def test_kernel_fault_is_contained_in_the_measuring_process():
+    """A faulting candidate (illegal address) kills every CUDA context of its
+    process on the device, so candidates run in a child measuring process: the
+    fault comes back as a status, the parent's torch tensors and cost-model
+    state stay valid, and measurement carries on in a fresh child."""
     import numpy as np
     import torch
     from paper_2006_06762_b200 import measure
-    from paper_2006_06762_b200 import runtime as rt
     from paper_2006_06762_b200.model import GpuCostModel
     from paper_2006_06762_b200.state import build, naive_program
     r = measure.configure(device=0, cache_dir="")
@@ -163,30 +144,15 @@ def test_kernel_fault_is_contained_in_the_runner_context():
         x = torch.arange(1 << 20, dtype=torch.float32, device="cuda")
         m = GpuCostModel(base=1.0)
         s0 = m.predict_batch([p])
-        gen0 = r.lib.lt_runner_generation(0)
-        mod = r.lib.lt_module_load(0, FAULT_PTX, len(FAULT_PTX))
-        assert mod, r.lib.lt_last_error()
-        fn = r.lib.lt_module_function(mod, b"lt_fault")
-        task = r.context(dag, 0).task
-        launches = (rt.Launch * 1)()
-        launches[0].func = fn
-        launches[0].grid[:] = (1, 1, 1)
-        launches[0].block[:] = (32, 1, 1)
-        launches[0].n_args = 0
-        rec = rt.MeasureRecord()
-        empty_i = np.zeros(1, np.int32)
-        empty_l = np.zeros(1, np.int64)
-        rt.check(r.lib.lt_measure(task, ctypes.addressof(launches), 1, rt.ptr(empty_i, rt.c_i32p),
-                                  rt.ptr(empty_l, rt.c_i64p), 0, 1, 5, 1.0, ctypes.addressof(rec)), "lt_measure")
-        assert rec.status == 2 and b"kernel fault" in rec.detail
-        r.reset_device()
-        assert r.lib.lt_runner_generation(0) == gen0 + 1
-        assert r.stats["device_resets"] == 1
-        torch.cuda.synchronize()                                  # the primary context is healthy
+        pid0 = r.pid
+        status, detail = r.inject_fault()
+        assert status == 2 and "kernel fault" in detail, detail
+        assert r.stats["device_faults"] == 1
+        torch.cuda.synchronize()                                  # the parent's CUDA state is healthy
         assert float(x[-1]) == float((1 << 20) - 1)
         assert np.array_equal(m.predict_batch([p]), s0)
-        (b,) = r.measure_programs([p])          # same kernel: reloaded from the kept image
-        assert b.status == "valid"
+        (b,) = r.measure_programs([p])                           # a fresh measuring process
+        assert b.status == "valid" and r.pid != pid0 and r.stats["restarts"] == 1
     finally:
         measure._shutdown()
 
@@ -196,11 +162,11 @@ def test_naive_multi_point_steps_verify():
     grid-stride step, guarded loads and stores for the tail) verifies on naive
     stream candidates, reductions and fused padding included."""
     from bench import load_stream
-    from paper_2006_06762_b200 import measure, ptxgen
+    from paper_2006_06762_b200 import measure
     from paper_2006_06762_b200.state import replay
-    r = measure.configure(device=0, cache_dir="", lower_workers=1)   # lower in-process
-    old = ptxgen.NAIVE_POINTS
-    ptxgen.NAIVE_POINTS = 4
+    old = os.environ.get("LT_NAIVE_POINTS")
+    os.environ["LT_NAIVE_POINTS"] = "4"             # read by ptxgen in the measuring process
+    r = measure.configure(device=0, cache_dir="", lower_workers=1)   # lower in that process
     try:
         for cfg in ("RC", "G10", "CL"):
             dag, stream = load_stream(cfg)
@@ -210,7 +176,10 @@ def test_naive_multi_point_steps_verify():
             assert naive, cfg
             assert all(x.status == "valid" for x in recs), [(x.status, x.detail) for x in recs]
     finally:
-        ptxgen.NAIVE_POINTS = old
+        if old is None:
+            os.environ.pop("LT_NAIVE_POINTS")
+        else:
+            os.environ["LT_NAIVE_POINTS"] = old
         measure._shutdown()
 
 

@@ -11,7 +11,7 @@ dag, st = load_stream(cfg)
 p = replay(dag, st[int(i)])
 outs = {}
 for be in ("nvrtc", "ptx"):
-    r = measure.configure(device=0, cache_dir="", backend=be)
+    r = measure.RunnerCore(device=0, cache_dir="", backend=be)
     (rec,) = r.measure_programs([p])
     ctx = r.context(dag, 0)
     name = dag.outputs[0]

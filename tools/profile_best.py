@@ -30,7 +30,7 @@ def best_candidate(cfg: str, n: int, offset: int = 0) -> None:
     from paper_2006_06762_b200 import runtime as rt
     from paper_2006_06762_b200.state import replay
     dag, stream = load_stream(cfg)
-    runner = measure.configure(device=0, cache_dir="")
+    runner = measure.RunnerCore(device=0, cache_dir="")
     progs = [replay(dag, h) for h in stream[offset:offset + n]]
     recs = runner.measure_programs(progs)
     best = min((r.cost_us, i) for i, r in enumerate(recs) if r.status == "valid")

@@ -7,7 +7,7 @@ import torch
 from hand_states import states
 from paper_2006_06762_b200 import measure, runtime as rt
 name, p = states()[int(sys.argv[1])]
-r = measure.configure(device=0, cache_dir="")
+r = measure.RunnerCore(device=0, cache_dir="")
 (rec,) = r.measure_programs([p])
 print(name, rec.status, rec.cost_us, flush=True)
 lo = r.lower(p)

@@ -23,7 +23,7 @@ def main() -> None:
     cfg = sys.argv[1]
     best = json.load(open(os.path.join(ROOT, "profiles", "tuned_best_histories.json")))[cfg]
     p = replay(config_dag(cfg), history_from_json(best["history"]))
-    r = measure.configure(device=0, cache_dir="")
+    r = measure.RunnerCore(device=0, cache_dir="")
     (rec,) = r.measure_programs([p])
     lo = r.lower(p)
     print(json.dumps({"config": cfg, "status": rec.status, "us": rec.cost_us,
