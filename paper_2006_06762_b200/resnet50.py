@@ -10,7 +10,10 @@ classifier.  Each is built with the reference's own builders (`conv2d`,
 
 from __future__ import annotations
 
+from .state import Bin, ComputeDAG, Const, IterVal, Lin, Read, Reduce, compute, placeholder
 from .state.workloads import build
+
+v = Lin.var
 
 # (input H=W, Ci, Co, kernel, stride, pad, count)
 CONVS = [
@@ -40,13 +43,47 @@ CONVS = [
 ]
 
 
-def tasks(batch: int = 16):
+def max_pool(n: int = 16, h: int = 112, c: int = 64, kernel: int = 3, stride: int = 2, pad: int = 1):
+    """M[n,y,x,c] = max over a kernel x kernel window of the padded input.
+
+    The pad stage mirrors the reference's conv padding (`src/workloads.py:45-67`,
+    a `Select` over the in-bounds test); its fill is 0, which equals
+    max-pooling's -inf padding here because the pooled tensor is a ReLU output
+    (>= 0) and every window holds at least one real element."""
+    from .state import Select
+    hp = h + 2 * pad
+    ho = (hp - kernel) // stride + 1
+    inb = Bin("mul",
+              Bin("mul", Bin("ge", IterVal(v("ph")), Const(float(pad))), Bin("lt", IterVal(v("ph")), Const(float(h + pad)))),
+              Bin("mul", Bin("ge", IterVal(v("pw")), Const(float(pad))), Bin("lt", IterVal(v("pw")), Const(float(h + pad)))))
+    x = placeholder("x", (n, h, h, c), iters=("x0", "x1", "x2", "x3"))
+    pnode = compute("P", (("pn", n), ("ph", hp), ("pw", hp), ("pc", c)),
+                    Select(inb, Read("x", (v("pn"), v("ph").shift(-pad), v("pw").shift(-pad), v("pc"))), Const(0.0)))
+    body = Reduce("max", ("rh", "rw"), Read("P", (v("mn"), v("mh").scale(stride) + v("rh"),
+                                                  v("mw").scale(stride) + v("rw"), v("mc"))))
+    m = compute("M", (("mn", n), ("mh", ho), ("mw", ho), ("mc", c)), body, reduce=(("rh", kernel), ("rw", kernel)))
+    return ComputeDAG((x, pnode, m))
+
+
+def global_avg_pool(n: int = 16, h: int = 7, c: int = 2048):
+    """G[n,c] = (sum over the h x h window) * 1/h²: a sum reduction and a scale."""
+    x = placeholder("x", (n, h, h, c), iters=("x0", "x1", "x2", "x3"))
+    s = compute("S", (("sn", n), ("sc", c)), Reduce("sum", ("rh", "rw"), Read("x", (v("sn"), v("rh"), v("rw"), v("sc")))),
+                reduce=(("rh", h), ("rw", h)))
+    g = compute("G", (("gn", n), ("gc", c)), Bin("mul", Read("S", (v("gn"), v("gc"))), Const(1.0 / (h * h))))
+    return ComputeDAG((x, s, g))
+
+
+def tasks(batch: int = 16, pools: bool = True):
     """[(name, dag, weight)] for every distinct subgraph."""
     out = []
     for h, ci, co, k, s, p, cnt in CONVS:
         name = f"conv{h}_{ci}_{co}_k{k}s{s}"
         out.append((name, build("conv2d", h=h, w=h, ci=ci, co=co, kernel=k, stride=s, pad=p, n=batch), cnt))
     out.append(("dense2048_1000", build("matmul", n=batch, m=1000, k=2048), 1))
+    if pools:
+        out.append(("maxpool112_64_k3s2", max_pool(n=batch), 1))
+        out.append(("avgpool7_2048", global_avg_pool(n=batch), 1))
     return out
 
 
