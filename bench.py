@@ -380,7 +380,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="RC", choices=sorted(FLOPS))
-    ap.add_argument("--batch", type=int, default=32, help="candidates per rank per step")
+    ap.add_argument("--batch", type=int, default=64, help="candidates per rank per step")
     ap.add_argument("--cpu-seconds", type=float, default=30.0,
                     help="cap on one reference candidate's CPU time (capped ones count as measured)")
     ap.add_argument("--sub-configs", default="G10,CL", help="extra configs measured in the same run ('' = none)")

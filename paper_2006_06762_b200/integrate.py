@@ -33,10 +33,12 @@ launch shape (the reference's CPU-oriented draws give ~1-2% of those for tiled
 sketches), then runs the reference's `sample_program` on that State.  This
 changes the search distribution and is off by default.
 
-Opt-in (`gpu_sketch_policy(loomtune, task)`): a task keeps
-only the sketches derived through a GPU rule (multi-level tiling — every tiled
-kernel stages its operands through shared memory, the cache-read rule — or
-reduction factorization, lowered as a cross-thread reduction).
+Opt-in (`gpu_sketch_policy(loomtune, task, gpu_rules=True)`, SURVEY.md §8(f)
+row 3): the task's sketches are derived with the paper's two GPU rules added to
+the reference's rule table (`sketch_rules.py`: a shared-memory caching node for
+computed operands, a cross-thread reduction) and only the sketches derived
+through a GPU rule are kept (multi-level tiling — every tiled kernel stages its
+operands through shared memory — reduction factorization, or the two GPU rules).
 """
 
 from __future__ import annotations
@@ -48,8 +50,12 @@ from .model import GpuCostModel
 from .replay import cmd_replay
 
 
-def make_evolve_batched(ev):
-    """Build the batched twin of `ev.evolve` from the reference module `ev`."""
+def make_evolve_batched(ev, score_population=None):
+    """Build the batched twin of `ev.evolve` from the reference module `ev`.
+
+    `score_population(model, programs) -> fitness list` replaces the default
+    one-pass `model.predict_batch(programs)` (the sharded scorer under
+    torch.distributed, `dist.score_batch_sharded`)."""
 
     def evolve_batched(initial, model, config, rng=None, stats=None):
         if not initial:
@@ -61,7 +67,7 @@ def make_evolve_batched(ev):
         gm = model if hasattr(model, "predict_batch") else GpuCostModel.wrap(model)
 
         def score(programs):
-            fits = gm.predict_batch(programs)
+            fits = score_population(gm, programs) if score_population else gm.predict_batch(programs)
             return [ev.Candidate(p, float(f)) for p, f in zip(programs, fits)]
 
         pool: dict = {}
@@ -191,40 +197,69 @@ def make_gpu_sampler(sample_program, tries: int = 64, factor_tries: int = 2048):
     return sample
 
 
-# rule ids of the reference's sketch rules that give a stage a GPU kernel shape
-# (src/sketch.py:260-329): multi-level tiling, tiling with fusion, reduction
-# factorization (lowered as a cross-thread reduction, ptxgen._xreduce)
-GPU_SKETCH_RULES = frozenset((3, 4, 6))
+# rule ids that give a stage a GPU kernel shape: the reference's multi-level
+# tiling, tiling with fusion and reduction factorization (src/sketch.py:260-329;
+# lowered as a cross-thread reduction, ptxgen._xreduce), and the paper's two GPU
+# rules (sketch_rules.py: shared-memory caching node, cross-thread reduction)
+GPU_SKETCH_RULES = frozenset((3, 4, 6, "gpu_smem", "gpu_ctr"))
 
 
-def gpu_sketch_policy(loomtune, task, structure: str = "SSSRRSRS") -> list:
+def gpu_sketch_policy(loomtune, task, structure: str = "SSSRRSRS", gpu_rules: bool = False) -> list:
     """Opt-in GPU sketch policy: Ansor's GPU sketches
     always tile a data-reuse stage (multi-level tiling staged through shared
     memory) or bind a factored reduction to threads; the reference's CPU rule
     table also keeps the untiled derivations (rule 1 `skip` on every node).
-    Keeps, in place and in order, the task's sketches whose rule path uses a GPU
-    rule, when there is one; returns the kept rule paths.  Changes the search
-    space, so it is off by default."""
+
+    gpu_rules: derive the task's sketches again with the paper's two GPU rules
+    added to the reference's rule table (`sketch_rules.GPU_RULES` through
+    `generate_sketches(extra_rules=...)`).  Then keeps, in place and in order,
+    the sketches whose rule path uses a GPU rule, when there is one; returns
+    the kept rule paths.  Changes the search space, so it is off by default."""
     import importlib
     sk = importlib.import_module(loomtune.__name__ + ".sketch")
-    traced = sk.generate_sketches_traced(task.dag, structure=structure)
+    if gpu_rules:
+        from .sketch_rules import GPU_RULES
+        traced = sk.generate_sketches_traced(task.dag, extra_rules=GPU_RULES, structure=structure)
+        task.sketches[:] = [p for p, _ in traced]
+    else:
+        traced = sk.generate_sketches_traced(task.dag, structure=structure)
     if len(traced) != len(task.sketches):
         raise ValueError(f"task {task.name}: sketch list does not match its rule paths")
-    keep = [i for i, (_, path) in enumerate(traced)
-            if any(isinstance(r, int) and r in GPU_SKETCH_RULES for r in path)]
+    keep = [i for i, (_, path) in enumerate(traced) if any(r in GPU_SKETCH_RULES for r in path)]
     if keep and len(keep) < len(traced):
         task.sketches[:] = [task.sketches[i] for i in keep]
         return [traced[i][1] for i in keep]
     return [path for _, path in traced]
 
 
-def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_features: bool = False) -> dict:
+def _world() -> int:
+    try:
+        import torch.distributed as dist
+    except ImportError:
+        return 1
+    return dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+
+
+def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_features: bool = False,
+            sharded: bool | None = None, stand_in: dict | None = None) -> dict:
     """Rebind the reference's hot-path call sites; returns the originals.
 
     gpu_train: `train` fits its trees on the GPU (`gbdt.train`, bit-identical
     models; trees deeper than `gbdt.MAX_DEPTH` — the
     device kernel's frontier limit — are fitted by the reference's own `train`);
-    False keeps the reference's own `train` and only wraps its result."""
+    False keeps the reference's own `train` and only wraps its result.
+
+    sharded (default: a torch.distributed group with more than one rank is
+    initialised): every measurement batch (`dist.measure_batch_sharded`) and
+    every evolution population (`dist.score_batch_sharded`) is partitioned
+    across the ranks, one GPU each; only the (status, cost) records and the
+    fitness vector are all-gathered.  Every rank runs the same
+    deterministic scheduler on the same gathered results, so the tune is
+    identical on all ranks and to the single-GPU tune.
+
+    stand_in: device-free replacements for the two device calls, for the CPU
+    multi-process tests only — {"measure_records": fn(programs, seed) ->
+    [measure.Record], "score": fn(model, programs) -> fitness list}."""
     import importlib
     sched = importlib.import_module(loomtune.__name__ + ".sched")
     cli = importlib.import_module(loomtune.__name__ + ".cli")
@@ -263,10 +298,37 @@ def install(loomtune, gpu_sampler: bool = False, gpu_train: bool = True, gpu_fea
         return ref_write(self, record)
     logio.LogWriter.write = write
     cli.cmd_replay = cmd_replay         # wall-clock replay
-    sched.measure_batch = measure_batch
-    cli.measure_batch = measure_batch
+    stand_in = stand_in or {}
+    if sharded is None:
+        sharded = _world() > 1
+    score_population = None
+    mb = measure_batch
+    if sharded:
+        from . import dist as D
+        records = stand_in.get("measure_records")
+
+        def mb(programs, spec=None, limits=None, best_cost=None):
+            return D.measure_batch_sharded(programs, spec, limits, best_cost, measure_records=records)
+        scorer = stand_in.get("score")
+
+        def score_population(gm, programs):
+            if scorer is not None:
+                return D.score_batch_sharded(gm, programs, score_fn=lambda ps: scorer(gm, ps))
+            return D.score_batch_sharded(gm, programs)
+    elif stand_in:
+        if "measure_records" in stand_in:
+            from .measure import MeasureLimits, normalise
+
+            def mb(programs, spec=None, limits=None, best_cost=None):
+                lim = limits or MeasureLimits()
+                return normalise(stand_in["measure_records"](list(programs), lim.check_seed), best_cost,
+                                 lim.cost_ceiling)
+        if "score" in stand_in:
+            score_population = stand_in["score"]
+    sched.measure_batch = mb
+    cli.measure_batch = mb
     sched.train = train
-    sched.evolve = make_evolve_batched(ev)
+    sched.evolve = make_evolve_batched(ev, score_population)
     if gpu_sampler:
         sched.sample_program = make_gpu_sampler(orig["sample_program"])
     return orig

@@ -225,7 +225,8 @@ AUDIT = [("G5", 0, "naive"), ("G5", 3, "tiled sync"), ("G5", 7, "tiled cp.async 
 
 
 def _path_of(lo) -> str:
-    k = [k for k in lo.kernels if k.info.get("template") in ("tiled", "naive", "xreduce")][-1]
+    order = {"tiled": 0, "xreduce": 1, "naive": 2}
+    k = min(lo.kernels, key=lambda k: order.get(k.info.get("template"), 3))
     i = k.info
     if i["template"] != "tiled":
         return i["template"]

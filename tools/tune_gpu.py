@@ -1,6 +1,6 @@
 """Run the reference's unchanged tuner with the B200 hot path installed.
 
-  python tools/tune_gpu.py CFG BUDGET [SEED] [--gpu-sampler] [--gpu-features] [--gpu-sketches]
+  python tools/tune_gpu.py CFG BUDGET [SEED] [--gpu-sampler] [--gpu-features] [--gpu-sketches] [--gpu-rules]
 
 Imports `loomtune` from baseline/_ref (pip-installed copy of the reference;
 falls back to /root/reference when present), installs the drop-ins
@@ -38,7 +38,8 @@ def main() -> None:
     seed = int(sys.argv[3]) if len(sys.argv) > 3 and sys.argv[3].isdigit() else 0
     gpu_sampler = "--gpu-sampler" in sys.argv
     gpu_features = "--gpu-features" in sys.argv
-    gpu_sketches = "--gpu-sketches" in sys.argv
+    gpu_sketches = "--gpu-sketches" in sys.argv or "--gpu-rules" in sys.argv
+    gpu_rules = "--gpu-rules" in sys.argv
     name, kw = W.CONFIGS[cfg]
     dag = LT.ComputeDAG.from_json(W.build(name, **kw).to_json())
     runner = measure.configure(device=0, cache_dir="")
@@ -65,13 +66,14 @@ def main() -> None:
                              importlib.import_module("loomtune.ir").history_to_json(rec["history"]),
                              "cost": rec["cost"], "status": rec["status"], "iteration": rec["iteration"]})
     task = LT.make_task(cfg, dag, structure="SSSRRSRS")
-    paths = integrate.gpu_sketch_policy(LT, task) if gpu_sketches else None
+    paths = integrate.gpu_sketch_policy(LT, task, gpu_rules=gpu_rules) if gpu_sketches else None
     t0 = time.perf_counter()
     res = LT.tune([task], LT.Objective(), budget, LT.TuneSettings(), LT.SchedulerParams(), seed=seed, log_sink=sink)
     wall = time.perf_counter() - t0
     integrate.uninstall(LT, orig)
     best = task.best_cost
     out = {"config": cfg, "budget": budget, "seed": seed, "gpu_sampler": gpu_sampler, "gpu_features": gpu_features,
+           "gpu_rules": gpu_rules,
            "gpu_sketches": [list(map(str, p)) for p in paths] if paths else None, "wall_s": wall, "timers": timers,
            "measured": len(measured), "valid": sum(m["status"] == "valid" for m in measured),
            "best_us": best, "best_tflops": FLOPS[cfg] / (best * 1e-6) / 1e12,
@@ -79,7 +81,7 @@ def main() -> None:
            "best_history": importlib.import_module("loomtune.ir").history_to_json(task.best_program.history),
            "history": measured}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"tune_{cfg}.json"), "w") as fh:
+    with open(os.path.join(ROOT, "gpurun_out", f"tune_{cfg}_s{seed}{'_rules' if gpu_rules else ''}.json"), "w") as fh:
         json.dump(out, fh)
     print(json.dumps({k: v for k, v in out.items() if k not in ("history", "best_history", "latency_curve")}))
     print("latency curve (us):", [round(x, 1) for x in task.latency])

@@ -3,7 +3,7 @@ reference's unchanged multi-task `tune` (gradient task scheduler,
 `src/sched.py:276-375`) over every distinct ResNet-50 subgraph, with the B200
 hot path installed.
 
-  python tools/tune_network.py BUDGET [SEED] [--batch N] [--gpu-sampler] [--gpu-sketches] [--tasks K]
+  python tools/tune_network.py BUDGET [SEED] [--batch N] [--gpu-sampler] [--gpu-sketches] [--gpu-rules] [--tasks K]
 
 Tasks come from `paper_2006_06762_b200.resnet50.tasks` (23 conv shapes + the
 classifier, weights = instance counts).  Under torchrun each rank measures its
@@ -56,9 +56,8 @@ def main() -> None:
     sched = importlib.import_module("loomtune.sched")
     orig = integrate.install(LT, gpu_sampler=bool(opt.get("--gpu-sampler")),
                              gpu_features=bool(opt.get("--gpu-features")))
-    if world > 1:
-        from paper_2006_06762_b200 import dist as D
-        sched.measure_batch = D.measure_batch_sharded
+    # under torchrun install() shards every measurement batch and every evolution
+    # population across the ranks (dist.measure_batch_sharded / score_batch_sharded)
     timers = {"evolve": 0.0, "measure": 0.0, "train": 0.0}
 
     def timed(key, fn):
@@ -86,8 +85,8 @@ def main() -> None:
     for name, dag, weight in specs:
         ldag = LT.ComputeDAG.from_json(dag.to_json())
         tasks.append(LT.make_task(name, ldag, weight=float(weight), dnn="resnet50", structure="SSSRRSRS"))
-        if opt.get("--gpu-sketches"):
-            integrate.gpu_sketch_policy(LT, tasks[-1])
+        if opt.get("--gpu-sketches") or opt.get("--gpu-rules"):
+            integrate.gpu_sketch_policy(LT, tasks[-1], gpu_rules=bool(opt.get("--gpu-rules")))
     t_setup = time.perf_counter() - t0
     t0 = time.perf_counter()
     LT.tune(tasks, LT.Objective(), budget, LT.TuneSettings(batch_size=16), LT.SchedulerParams(), seed=seed,
