@@ -29,7 +29,7 @@ constexpr int MAX_NEST = 32;
 constexpr int MAX_LOOPS = 64;
 constexpr int MAX_ITERS = 24;
 constexpr int MAX_VIEWS = 12;
-constexpr int MAX_STACK = 48;
+constexpr int MAX_STACK = 32;
 
 struct Iv { long long lo, hi; };
 
@@ -432,6 +432,333 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
 #undef O
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-statement kernel (the default).  The thread-per-statement kernel
+// above keeps ~4 KB of per-statement scratch (decode stacks, intervals, per-view
+// statistics, working sets) in local memory, which at full occupancy spills to
+// HBM (r01 ncu: 7.4 KB read + 2.5 KB written per statement for 2.3 KB of
+// algorithmic bytes).  Here a warp owns one statement: the per-statement tables
+// live in shared memory and the lanes split the work — one lane per iterator
+// (masks, own-range intervals, the two stride evaluations), per view (access
+// statistics, reuse, stride), per nest position (working set, each lane
+// evaluating the intervals it needs on the fly), per intensity point and per
+// ranked buffer slot.  Every value is computed by exactly the expression the
+// thread kernel uses (same operand order, --fmad=false), so rows are identical.
+// A block of FW_WARPS warps stages FW_CHUNK rows in shared memory and writes
+// them out coalesced (column-major: FW_CHUNK consecutive statements per column).
+constexpr int FW_WARPS = 8;
+constexpr int FW_CHUNK = 32;
+constexpr int FW_LD = NF + 1;            // odd row stride: conflict-free lane-per-column access
+
+struct WarpScratch {
+  unsigned long long iter_mask[MAX_ITERS];
+  Iv iv[MAX_ITERS];
+  long long val0[MAX_ITERS], val1[MAX_ITERS];
+  unsigned long long present[MAX_VIEWS];
+  int vdims[MAX_VIEWS], vmarks[MAX_VIEWS], vhasw[MAX_VIEWS], vrank[MAX_VIEWS], vndims[MAX_VIEWS];
+  double tb[MAX_VIEWS], ub[MAX_VIEWS], ul[MAX_VIEWS], cnt[MAX_VIEWS], di[MAX_VIEWS], db[MAX_VIEWS],
+      strd[MAX_VIEWS];
+  int acc[MAX_VIEWS], reuse[MAX_VIEWS];
+  double ws[MAX_NEST];
+  int ok;
+};
+
+// interval of iterator `it` at nest position pos (pos < 0: own ranges)
+__device__ __forceinline__ Iv iter_interval(const int32_t* nodes, const int32_t* itab, const int32_t* loops, int it,
+                                            int pos, bool& ok) {
+  Iv r{0, 0};
+  ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, r);
+  return r;
+}
+
+__device__ __forceinline__ double wcol(int k, double x) {
+  return is_onehot(k) ? x : log2(1.0 + (x > 0.0 ? x : 0.0));
+}
+
+__device__ void warp_feature_row(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off, int64_t s,
+                                 double* __restrict__ row, WarpScratch& S, int* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* r = words + stmt_off[s];
+  const int n_nest = r[0], own_start = r[1], n_loops = r[2], n_iter = r[3], n_views = r[4];
+  const int unroll = r[5], n_live = r[6], has_reduce = r[7] & 1, gpu_feats = r[7] & 2;
+  const int32_t* ops = r + 8;
+  const int n_nodes = r[17];
+  if (n_nest > MAX_NEST || n_loops > MAX_LOOPS || n_iter > MAX_ITERS || n_views > MAX_VIEWS) {
+    for (int i = lane; i < NF; i += 32) row[i] = __longlong_as_double(0x7ff8000000000000ULL);
+    if (lane == 0) atomicExch(err, 1);
+    return;
+  }
+  const int32_t* nest = r + HDR;
+  const int32_t* loops = nest + 4 * n_nest;
+  const int32_t* itab = loops + 3 * n_loops;
+  const int32_t* nodes = itab + 2 * n_iter;
+  const int inner_own = (n_nest > own_start) ? nest[4 * (n_nest - 1) + 3] : -1;
+  bool ok = true;
+
+  // ---- lane per iterator: own-loop mask, own-range interval, stride evaluations
+  if (lane < n_iter) {
+    const int it = lane;
+    unsigned long long m = 0;
+    const int32_t* nd = nodes + 2 * itab[2 * it];
+    for (int n = 0; n < itab[2 * it + 1]; ++n)
+      if (nd[2 * n] == 0) m |= 1ULL << nd[2 * n + 1];
+    S.iter_mask[it] = m;
+    S.iv[it] = iter_interval(nodes, itab, loops, it, -1, ok);
+    if (inner_own >= 0) {
+      long long v0 = 0, v1 = 0;
+      ok &= ast_eval(nd, itab[2 * it + 1], -1, v0);
+      ok &= ast_eval(nd, itab[2 * it + 1], inner_own, v1);
+      S.val0[it] = v0;
+      S.val1[it] = v1;
+    }
+  }
+  // ---- lane 0: view record offsets (variable-length, sequential)
+  if (lane == 0) {
+    const int32_t* vp = nodes + 2 * n_nodes;
+    for (int v = 0; v < n_views; ++v) {
+      S.vmarks[v] = vp[0]; S.vhasw[v] = vp[1]; S.vrank[v] = vp[2]; S.vndims[v] = vp[3];
+      const int32_t* d = vp + 4;
+      S.vdims[v] = (int)(d - r);
+      for (int k = 0; k < vp[3]; ++k) d = dim_next(d);
+      vp = d;
+    }
+  }
+  __syncwarp();
+
+  double total = 1.0;
+  for (int i = 0; i < n_nest; ++i) total *= (double)nest[4 * i];
+  double red_prod = 1.0, alloc = 4.0;
+  for (int i = own_start; i < n_nest; ++i) {
+    if (nest[4 * i + 1] == 1) red_prod *= (double)nest[4 * i];
+    else alloc *= (double)nest[4 * i];
+  }
+  int ops_total = 0;
+  for (int k = 0; k < 9; ++k) ops_total += ops[k];
+
+  // ---- lane per view: access statistics, reuse, stride (src/features.py:202-259)
+  if (lane < n_views) {
+    const int v = lane;
+    const int32_t* d = r + S.vdims[v];
+    const int nd_ = S.vndims[v];
+    unsigned long long m = 0;
+    {
+      const int32_t* q = d;
+      for (int k = 0; k < nd_; ++k) {
+        for (int t = 0; t < q[4]; ++t) m |= S.iter_mask[q[5 + 2 * t]];
+        q = dim_next(q);
+      }
+    }
+    S.present[v] = m;
+    const bool has_w = S.vhasw[v] != 0;
+    const bool has_r = (S.vmarks[v] > S.vhasw[v]) || (has_w && red_prod > 1.0);
+    S.acc[v] = (has_w && has_r) ? 2 : (has_w ? 1 : 0);
+    long long uprod = 1, last = 1;
+    double lines = 1.0;
+    {
+      const int32_t* q = d;
+      for (int k = 0; k < nd_; ++k) {
+        long long wd = hull_width(q, S.iv);
+        uprod *= wd;
+        if (k < nd_ - 1) lines *= (double)wd; else last = wd;
+        q = dim_next(q);
+      }
+    }
+    S.ub[v] = (double)uprod * 4.0;
+    double lc = ceil((double)(last * 4) / 64.0);
+    S.ul[v] = lines * (lc > 1.0 ? lc : 1.0);
+    S.tb[v] = ((double)S.vmarks[v] * total) * 4.0;
+    int absent_last = -1;
+    double counter = 1.0;
+    for (int i = 0; i < n_nest; ++i) {
+      int oi = nest[4 * i + 3];
+      bool present = oi >= 0 && ((m >> oi) & 1ULL);
+      if (!present && nest[4 * i] > 1) { counter *= (double)nest[4 * i]; absent_last = i; }
+    }
+    if (has_w && has_reduce && red_prod > 1.0) {
+      S.reuse[v] = 1; S.cnt[v] = red_prod; S.di[v] = 1.0; S.db[v] = (double)(4 * S.vmarks[v]);
+    } else if (absent_last >= 0) {
+      S.reuse[v] = 0; S.cnt[v] = counter;
+      double dit = 1.0;
+      for (int i = absent_last + 1; i < n_nest; ++i) dit *= (double)nest[4 * i];
+      S.di[v] = dit; S.db[v] = (dit * 4.0) * (double)S.vmarks[v];
+    } else {
+      S.reuse[v] = 2; S.cnt[v] = 1.0; S.di[v] = 0.0; S.db[v] = 0.0;
+    }
+    double sv = 0.0;
+    if (inner_own >= 0 && ((m >> inner_own) & 1ULL)) {
+      long long a0 = 0, a1 = 0, fs = 1;
+      const int32_t* dd[16];
+      const int32_t* q = d;
+      int ndc = nd_ < 16 ? nd_ : 16;
+      for (int k = 0; k < ndc; ++k) { dd[k] = q; q = dim_next(q); }
+      for (int k = ndc - 1; k >= 0; --k) {
+        long long size = dd[k][0];
+        long long x0 = dim_value(dd[k], S.val0), x1 = dim_value(dd[k], S.val1);
+        x0 = x0 < 0 ? 0 : (x0 > size - 1 ? size - 1 : x0);
+        x1 = x1 < 0 ? 0 : (x1 > size - 1 ? size - 1 : x1);
+        a0 += x0 * fs; a1 += x1 * fs;
+        fs *= size;
+      }
+      long long dlt = a1 - a0;
+      sv = (double)((dlt < 0 ? -dlt : dlt) * 4);
+    }
+    S.strd[v] = sv;
+  }
+  // ---- lane per nest position: working set inside it (src/features.py:266-274)
+  for (int pos = lane; pos < n_nest; pos += 32) {
+    double acc_ws = 0.0;
+    for (int v = 0; v < n_views; ++v) {
+      long long pr = 1;
+      const int32_t* d = r + S.vdims[v];
+      for (int k = 0; k < S.vndims[v]; ++k) {
+        long long lo = d[3], hi = d[3];
+        for (int t = 0; t < d[4]; ++t) {
+          const Iv a = iter_interval(nodes, itab, loops, d[5 + 2 * t], pos, ok);
+          long long c = d[6 + 2 * t];
+          if (c >= 0) { lo += c * a.lo; hi += c * a.hi; }
+          else { lo += c * a.hi; hi += c * a.lo; }
+        }
+        int st = d[1], pext = d[2];
+        if (pext > 0) {
+          if (st > 1) { lo = fdiv(lo, st); hi = fdiv(hi, st); }
+          if (fdiv(lo, pext) == fdiv(hi, pext)) { lo = fmod_(lo, pext); hi = fmod_(hi, pext); }
+          else { lo = 0; hi = pext - 1; }
+        }
+        long long size = d[0];
+        long long l2 = lo > 0 ? lo : 0;
+        long long h2 = hi < size - 1 ? hi : size - 1;
+        long long w = h2 - l2 + 1;
+        pr *= (w > 1 ? w : 1);
+        d = dim_next(d);
+      }
+      acc_ws += (double)pr * 4.0;
+    }
+    S.ws[pos] = acc_ws;
+  }
+  __syncwarp();
+
+  // ---- row assembly (src/features.py:388-417), lanes over column groups
+  for (int k = lane; k < 9; k += 32) row[k] = wcol(k, (double)ops[k] * total);
+  for (int k = 9 + lane; k < 18; k += 32) row[k] = 0.0;
+  if (lane < 3) {                          // lane 0 vectorize, 1 unroll, 2 parallel block
+    double b[11];
+    const int base_col = lane == 0 ? 18 : (lane == 1 ? 29 : 40);
+    if (lane == 1) {
+      for (int k = 0; k < 11; ++k) b[k] = 0.0;
+      long long prod = 1;
+      int n_cov = 0, first = -1, tag = -1;
+      if (unroll > 0 && n_nest > own_start) {
+        for (int i = n_nest - 1; i >= own_start; --i) {
+          if (prod * nest[4 * i] > unroll) break;
+          prod *= nest[4 * i];
+          int p = position(nest, n_nest, i);
+          tag = (n_cov == 0) ? p : (tag == p ? tag : 7);
+          if (n_cov == 0) first = i;
+          ++n_cov;
+        }
+      }
+      if (!n_cov) b[1] = 1.0;
+      else { b[0] = (double)nest[4 * first]; b[1 + tag] = 1.0; b[9] = (double)prod; b[10] = (double)n_cov; }
+    } else {
+      annotation_block(nest, n_nest, lane == 0 ? 2 : 1, b);
+    }
+    for (int k = 0; k < 11; ++k) row[base_col + k] = wcol(base_col + k, b[k]);
+  }
+  if (lane >= 3 && lane < 11) {            // gpu_* slots
+    const int k = 51 + (lane - 3);
+    if (gpu_feats) row[k] = wcol(k, (double)(words + stmt_off[s + 1] - 8)[lane - 3]);
+    else row[k] = 0.0;                     // the reference leaves the gpu_* slots zero
+  }
+  if (lane >= 11 && lane < 21) {           // intensity curve point j
+    const int j = lane - 10;
+    if (n_nest == 0 || ops_total == 0) {
+      row[58 + j] = 0.0;
+    } else {
+      int depth = (int)ceil((double)j / 10.0 * (double)n_nest);
+      if (depth < 1) depth = 1;
+      const int pos = n_nest - depth;
+      double inside = 1.0;                 // same left-to-right product as inside[pos]
+      for (int i = n_nest - 1; i >= pos; --i) inside = inside * (double)nest[4 * i];
+      double by;
+      if (pos == 0) { by = 0.0; for (int v = 0; v < n_views; ++v) by += S.ub[v]; }
+      else by = S.ws[pos - 1];
+      double flops = (double)ops_total * inside;
+      row[58 + j] = wcol(58 + j, flops / (by > 1.0 ? by : 1.0));
+    }
+  }
+  if (lane >= 21 && lane < 26) {           // ranked buffer slot
+    const int slot = lane - 21;
+    const int o = 69 + 18 * slot;
+    const int n_rank = n_views < 5 ? n_views : 5;
+    if (slot >= n_rank) {
+      for (int k = 0; k < 18; ++k) row[o + k] = 0.0;
+    } else {
+      // the view of rank `slot` under (-total_bytes, name)
+      int v = -1;
+      for (int u = 0; u < n_views && v < 0; ++u) {
+        int before = 0;
+        for (int w2 = 0; w2 < n_views; ++w2)
+          if (S.tb[w2] > S.tb[u] || (S.tb[w2] == S.tb[u] && S.vrank[w2] < S.vrank[u])) ++before;
+        if (before == slot) v = u;
+      }
+      for (int k = 0; k < 3; ++k) row[o + k] = (k == S.acc[v]) ? 1.0 : 0.0;
+      double ln = S.tb[v] / 64.0;
+      row[o + 3] = wcol(o + 3, S.tb[v]); row[o + 4] = wcol(o + 4, S.ub[v]);
+      row[o + 5] = wcol(o + 5, ln); row[o + 6] = wcol(o + 6, S.ul[v]);
+      for (int k = 0; k < 3; ++k) row[o + 7 + k] = (k == S.reuse[v]) ? 1.0 : 0.0;
+      row[o + 10] = wcol(o + 10, S.di[v]); row[o + 11] = wcol(o + 11, S.db[v]);
+      row[o + 12] = wcol(o + 12, S.cnt[v]); row[o + 13] = wcol(o + 13, S.strd[v]);
+      double c = S.cnt[v] > 1.0 ? S.cnt[v] : 1.0;
+      row[o + 14] = wcol(o + 14, S.tb[v] / c); row[o + 15] = wcol(o + 15, S.ub[v] / c);
+      row[o + 16] = wcol(o + 16, ln / c); row[o + 17] = wcol(o + 17, S.ul[v] / c);
+    }
+  }
+  if (lane == 26) {
+    row[159] = wcol(159, alloc);
+    row[160] = wcol(160, (double)n_live);
+    row[161] = wcol(161, (double)n_nest);
+    row[162] = wcol(162, total);
+    row[163] = wcol(163, (double)unroll);
+  }
+  const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+  __syncwarp();
+  if (bad) {
+    for (int i = lane; i < NF; i += 32) row[i] = __longlong_as_double(0x7ff8000000000000ULL);
+    if (lane == 0) atomicExch(err, 2);
+  }
+}
+
+__global__ void __launch_bounds__(FW_WARPS * 32)
+features_warp_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ stmt_off, int64_t n_stmt,
+                     double* __restrict__ out, int64_t ld_col, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char fw_smem[];
+  double* rows = (double*)fw_smem;                                     // FW_CHUNK x FW_LD
+  WarpScratch* scratch = (WarpScratch*)(rows + FW_CHUNK * FW_LD);
+  const int warp = threadIdx.x >> 5;
+  WarpScratch& S = scratch[warp];
+  for (int64_t s0 = (int64_t)blockIdx.x * FW_CHUNK; s0 < n_stmt; s0 += (int64_t)gridDim.x * FW_CHUNK) {
+    const int here = (int)min((int64_t)FW_CHUNK, n_stmt - s0);
+    for (int i = warp; i < here; i += FW_WARPS) {
+      warp_feature_row(words, stmt_off, s0 + i, rows + i * FW_LD, S, err);
+      __syncwarp();
+    }
+    __syncthreads();
+    if (ld_col == 1) {                     // rows[n][164]: the chunk is one contiguous run
+      double* dst = out + s0 * NF;
+      for (int e = threadIdx.x; e < here * NF; e += blockDim.x) {
+        const int i = e / NF, k = e - i * NF;
+        dst[e] = rows[i * FW_LD + k];
+      }
+    } else {                               // cols[164][n]: `here` consecutive statements per column
+      for (int e = threadIdx.x; e < here * NF; e += blockDim.x) {
+        const int k = e / here, i = e - k * here;
+        out[(int64_t)k * ld_col + s0 + i] = rows[i * FW_LD + k];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Persistent grid-stride loop: the grid is sized so that each thread's local
 // working set (intervals, per-view statistics, decode stacks) stays L1/L2
 // resident instead of spilling to HBM (SM count x blocks_per_sm blocks).
@@ -448,6 +775,28 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
 static int launch_features(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt, double* d_out,
                            int64_t ld_col, int* d_err, void* stream) {
   if (n_stmt <= 0) return 0;
+  if (getenv("LT_FEATURES_THREAD") == nullptr) {
+    static int wsms = -1, wdev = -1;
+    const size_t smem = (size_t)lt::FW_CHUNK * lt::FW_LD * sizeof(double) + lt::FW_WARPS * sizeof(lt::WarpScratch);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != wdev) {
+      cudaDeviceGetAttribute(&wsms, cudaDevAttrMultiProcessorCount, dev);
+      if (lt::check_cuda(cudaFuncSetAttribute(lt::features_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem), "features smem attr"))
+        return -1;
+      wdev = dev;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lt::features_warp_kernel, lt::FW_WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    int64_t chunks = (n_stmt + lt::FW_CHUNK - 1) / lt::FW_CHUNK;
+    int64_t blocks = (int64_t)wsms * per_sm;
+    if (blocks > chunks) blocks = chunks;
+    lt::features_warp_kernel<<<(unsigned)blocks, lt::FW_WARPS * 32, smem, (cudaStream_t)stream>>>(
+        d_words, d_stmt_off, n_stmt, d_out, ld_col, d_err);
+    return lt::check_launch("features_warp_kernel");
+  }
   const int threads = 128;
   static int sms = 0, per_sm = 0;
   if (!sms) {

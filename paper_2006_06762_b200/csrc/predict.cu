@@ -7,14 +7,21 @@
 //     order (the product is precomputed on the host with the same IEEE multiply);
 //   * per program: numpy's add.reduce order over its rows (plain loop below 8
 //     rows, numpy's 8-accumulator pairwise scheme above).
-// Layout: the model's nodes live in global memory read through the read-only
-// path (61 KB at 30 trees x 127 nodes; L1-resident).  Each block stages a tile of
-// rows into shared memory with coalesced loads, restricted to the feature columns
-// the model actually tests, then each thread walks all trees for one row.
+// Layout (predict_trees_kernel, the default): one tree per warp.  Each block
+// copies the whole model into shared memory once (16 B per node: 61 KB at 30
+// trees x 127 nodes) and loops over tiles of TILE_ROWS rows (persistent grid):
+// the tile's tested feature columns are staged into shared memory with
+// coalesced loads; warp w walks trees w, w+W, ... for the tile's rows (one row
+// per lane), every level a shared-memory node load and a shared-memory feature
+// load, and writes each (tree, row) leaf into a shared partials table; then one
+// thread per row adds base + partials in tree order — the reference's
+// summation order, so results are bit-identical.  Models too large for shared
+// memory use predict_rows_kernel (thread per row, nodes read through L1).
 // Compiled with --fmad=false.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <vector>
 #include <string>
 #include "common.h"
@@ -33,6 +40,7 @@ struct Node {
 
 struct Model {
   int n_trees = 0;
+  int n_nodes = 0;
   int n_used = 0;          // compact feature columns
   double base = 0.0;
   Node* d_nodes = nullptr;
@@ -74,6 +82,56 @@ predict_rows_kernel(const double* __restrict__ X, int64_t n_rows, bool col_major
     acc = __dadd_rn(acc, cur.x);
   }
   out[row0 + r] = acc;
+}
+
+constexpr int TILE_ROWS = 64;
+constexpr int TREE_WARPS = 16;
+
+__global__ void __launch_bounds__(TREE_WARPS * 32)
+predict_trees_kernel(const double* __restrict__ X, int64_t n_rows, bool col_major, const Node* __restrict__ nodes,
+                     int n_nodes, const int32_t* __restrict__ tree_off, int n_trees,
+                     const int32_t* __restrict__ used, int n_used, double base, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Node* s_nodes = (Node*)smem_raw;                                   // n_nodes
+  double* tile = (double*)(s_nodes + n_nodes);                       // n_used x TILE_ROWS (column-major)
+  double* part = tile + (size_t)n_used * TILE_ROWS;                  // n_trees x TILE_ROWS
+  int32_t* s_off = (int32_t*)(part + (size_t)n_trees * TILE_ROWS);   // n_trees + 1
+  for (int i = threadIdx.x; i < n_nodes; i += blockDim.x) s_nodes[i] = nodes[i];
+  for (int i = threadIdx.x; i <= n_trees; i += blockDim.x) s_off[i] = tree_off[i];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t row0 = (int64_t)blockIdx.x * TILE_ROWS; row0 < n_rows; row0 += (int64_t)gridDim.x * TILE_ROWS) {
+    const int rows_here = (int)min((int64_t)TILE_ROWS, n_rows - row0);
+    __syncthreads();                      // previous tile fully consumed (and the model staged)
+    if (col_major) {                      // X[164][n_rows]: a column's rows are contiguous
+      for (int e = threadIdx.x; e < n_used * TILE_ROWS; e += blockDim.x) {
+        const int c = e / TILE_ROWS, r = e - c * TILE_ROWS;
+        if (r < rows_here) tile[e] = X[(int64_t)used[c] * n_rows + row0 + r];
+      }
+    } else {
+      for (int e = threadIdx.x; e < n_used * TILE_ROWS; e += blockDim.x) {
+        const int r = e / n_used, c = e - r * n_used;
+        if (r < rows_here) tile[c * TILE_ROWS + r] = X[(row0 + r) * NF + used[c]];
+      }
+    }
+    __syncthreads();
+    for (int t = warp; t < n_trees; t += TREE_WARPS) {
+      const Node* nd = s_nodes + s_off[t];
+      for (int r = lane; r < rows_here; r += 32) {
+        Node cur = nd[0];
+        for (int lvl = 0; lvl < 64 && cur.feat >= 0; ++lvl) {
+          const int nxt = (tile[cur.feat * TILE_ROWS + r] <= cur.x) ? (cur.lr & 0xffff) : (cur.lr >> 16);
+          cur = nd[nxt];
+        }
+        part[t * TILE_ROWS + r] = cur.x;
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < rows_here; r += blockDim.x) {
+      double acc = base;
+      for (int t = 0; t < n_trees; ++t) acc = __dadd_rn(acc, part[t * TILE_ROWS + r]);
+      out[row0 + r] = acc;
+    }
+  }
 }
 
 __global__ void segment_sum_kernel(const double* __restrict__ row_scores, const int64_t* __restrict__ prog_off,
@@ -131,6 +189,7 @@ int64_t lt_model_create(int n_trees, const int64_t* tree_node_off, const int32_t
   if (used.empty()) used.push_back(0);
   Model* m = new Model();
   m->n_trees = n_trees;
+  m->n_nodes = (int)nodes.size();
   m->n_used = (int)used.size();
   m->base = base;
   if (lt::check_cuda(cudaMalloc(&m->d_nodes, nodes.size() * sizeof(Node)), "cudaMalloc nodes") ||
@@ -163,11 +222,51 @@ int lt_model_info(int64_t handle, int* n_trees, int* n_used_features) {
   return 0;
 }
 
+static int device_props(int* sms, size_t* smem_optin) {
+  static int cached_dev = -1, cached_sms = 0;
+  static size_t cached_smem = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int v = 0;
+    cudaDeviceGetAttribute(&cached_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cached_smem = (size_t)v;
+    cached_dev = dev;
+  }
+  *sms = cached_sms;
+  *smem_optin = cached_smem;
+  return dev;
+}
+
 static int predict_device(int64_t handle, const double* d_rows, int64_t n_rows, bool col_major,
                           double* d_row_scores, void* stream) {
   Model* m = (Model*)(intptr_t)handle;
   if (!m) return lt::fail("null model");
   if (n_rows <= 0) return 0;
+  int sms = 0;
+  size_t optin = 0;
+  const int tdev = device_props(&sms, &optin);
+  const size_t tsmem = (size_t)m->n_nodes * sizeof(Node) +
+                       (size_t)(m->n_used + m->n_trees) * lt::TILE_ROWS * sizeof(double) +
+                       (size_t)(m->n_trees + 1) * sizeof(int32_t);
+  if (tsmem <= optin && getenv("LT_PREDICT_THREAD_PER_ROW") == nullptr) {
+    static size_t tconfigured[64] = {};
+    if (tsmem > 48 * 1024 && (tdev < 0 || tdev >= 64 || tsmem > tconfigured[tdev])) {
+      if (lt::check_cuda(cudaFuncSetAttribute(lt::predict_trees_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)tsmem), "smem attr"))
+        return -1;
+      if (tdev >= 0 && tdev < 64) tconfigured[tdev] = tsmem;
+    }
+    const int per_sm = tsmem <= optin / 2 ? 2 : 1;
+    int64_t tiles = (n_rows + lt::TILE_ROWS - 1) / lt::TILE_ROWS;
+    int64_t blocks = (int64_t)sms * per_sm;
+    if (blocks > tiles) blocks = tiles;
+    lt::predict_trees_kernel<<<(unsigned)blocks, lt::TREE_WARPS * 32, tsmem, (cudaStream_t)stream>>>(
+        d_rows, n_rows, col_major, m->d_nodes, m->n_nodes, m->d_tree_off, m->n_trees, m->d_used, m->n_used,
+        m->base, d_row_scores);
+    return lt::check_launch("predict_trees_kernel");
+  }
   size_t smem = (size_t)lt::ROWS_PER_BLOCK * (m->n_used + 1) * sizeof(double);
   // the opt-in shared-memory grant is per device (function attributes are per context)
   static size_t configured[64] = {};

@@ -116,3 +116,40 @@ def test_opt_in_gpu_feature_slots(corpus):
             nb, nt, nv, smem = gpu_binding(p, s)
             want = np.log2(1.0 + np.asarray([nb, 1, 1, nt, 1, 1, nv, smem], np.float64))
             assert np.allclose(row[51:59], want, rtol=0, atol=1e-12)
+
+
+def _stream_programs(n_per_cfg=256):
+    import bench
+    from paper_2006_06762_b200.state import replay
+    progs = []
+    for cfg in ("RC", "CL", "G10", "TBG"):
+        dag, stream = bench.load_stream(cfg)
+        progs += [replay(dag, h) for h in stream[:n_per_cfg]]
+    return progs
+
+
+def test_warp_and_thread_feature_kernels_agree_bitwise(corpus, monkeypatch):
+    """The warp-per-statement kernel (default) and the thread-per-statement
+    kernel compute every row identically (golden corpus + stream States)."""
+    from paper_2006_06762_b200.features import extract_features_batch
+    progs = list(corpus.programs) + _stream_programs()
+    warp = extract_features_batch(progs)
+    monkeypatch.setenv("LT_FEATURES_THREAD", "1")
+    thread = extract_features_batch(progs)
+    monkeypatch.delenv("LT_FEATURES_THREAD")
+    for i, (a, b) in enumerate(zip(warp, thread)):
+        assert np.array_equal(a, b), i
+
+
+def test_tree_per_warp_and_thread_per_row_predict_agree_bitwise(corpus, monkeypatch):
+    """One-tree-per-warp predict (default, model in shared memory) equals the
+    thread-per-row kernel bit for bit, and both equal the golden scores."""
+    from paper_2006_06762_b200.model import GpuCostModel
+    m = GpuCostModel.from_json(corpus.model_json)
+    progs = list(corpus.programs) + _stream_programs()
+    a = m.predict_batch(progs)
+    monkeypatch.setenv("LT_PREDICT_THREAD_PER_ROW", "1")
+    b = m.predict_batch(progs)
+    monkeypatch.delenv("LT_PREDICT_THREAD_PER_ROW")
+    assert np.array_equal(a, b)
+    assert np.array_equal(a[:len(corpus.scores)], corpus.scores)

@@ -1,4 +1,5 @@
-"""Profile the best program the tuner found per operator (profiles/tuned_best_histories.json):
+"""Profile the best program the tuner found per operator (profiles/r02_tuned_best.json, or the
+file named by LT_TUNED_BEST):
 measure it through the runner, then relaunch its kernels 3x inside NVTX range "profile".
 
   ncu --set full --nvtx --nvtx-include "profile/" ... python tools/profile_tuned.py CFG
@@ -21,7 +22,7 @@ def main() -> None:
     from paper_2006_06762_b200 import runtime as rt
     from paper_2006_06762_b200.state import config_dag, history_from_json, replay
     cfg = sys.argv[1]
-    best = json.load(open(os.path.join(ROOT, "profiles", "tuned_best_histories.json")))[cfg]
+    best = json.load(open(os.environ.get("LT_TUNED_BEST", os.path.join(ROOT, "profiles", "r02_tuned_best.json"))))[cfg]
     p = replay(config_dag(cfg), history_from_json(best["history"]))
     r = measure.RunnerCore(device=0, cache_dir="")
     (rec,) = r.measure_programs([p])
