@@ -30,8 +30,9 @@ def main() -> None:
     print(json.dumps({"config": cfg, "status": rec.status, "us": rec.cost_us,
                       "tflops": FLOPS[cfg] / (rec.cost_us * 1e-6) / 1e12 if rec.status == "valid" else None,
                       "tuned_us": best["best_us"], "kernels": [k.info for k in lo.kernels]}), flush=True)
-    key = hashlib.sha1(lo.source.encode()).hexdigest()
-    funcs = r.load(key, b"", [k.entry for k in lo.kernels])
+    funcs = []
+    for ents, text, opts in measure._modules_of(lo):
+        funcs += r.load(hashlib.sha1((opts or "").encode() + text.encode()).hexdigest(), b"", ents)
     ctx = r.context(p.dag, 0)
     launches = ctx._launches(lo, funcs)
     torch.cuda.synchronize()
