@@ -144,6 +144,24 @@ int lt_measure(int64_t task, const lt_launch* launches, int n_launch, const int3
                const int64_t* numel, int n_check, int min_repeat, int max_repeat, double min_ms,
                lt_measure_record* rec);
 
+/* ---- multi-GPU exchange ---------------------------
+ * One process per GPU; each measures its shard of a batch (lt_measure) and
+ * scores its shard of a population (lt_score_batch); only fixed-size records,
+ * the fitness vector and the serialised model cross GPUs, over NCCL (opened at
+ * run time: libnccl.so.2).  Replaces nothing in the reference (single process,
+ * src/machine.py:257-274 and src/evolve.py:453-454 are serial loops); the
+ * Python path does the same exchange with torch.distributed (dist.py).
+ * Shards are padded to the largest shard: out has world * n_local_max entries. */
+int lt_comm_unique_id(char* out128);                      /* rank 0, sent to the others out of band */
+int64_t lt_comm_create(const char* id128, int rank, int world, int device);
+void lt_comm_destroy(int64_t comm);
+int lt_comm_rank(int64_t comm, int* rank, int* world);
+int lt_comm_allgather(int64_t comm, const void* local, int64_t bytes_per_rank, void* out);
+int lt_comm_allgather_records(int64_t comm, const lt_measure_record* local, int64_t n_local_max,
+                              lt_measure_record* out);
+int lt_comm_allgather_f64(int64_t comm, const double* local, int64_t n_local_max, double* out);
+int lt_comm_broadcast(int64_t comm, void* buf, int64_t bytes, int root);   /* e.g. the model after train */
+
 /* FP32 FFMA peak of the device (TFLOP/s), the roofline denominator for candidate kernels. */
 int lt_ffma_peak(int device, double* tflops, double* ms);
 /* Same with register (non-immediate) FFMA operands: the GEMM inner-product form. */

@@ -15,6 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
+INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(LIBDIR, "libloomtune_b200.so")
 WORKER = os.path.join(LIBDIR, "lt_nvrtc_worker")
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
@@ -28,6 +29,7 @@ SOURCES = {
     "gbdt.cu": ["--fmad=false"],
     "api.cu": [],
     "runner.cu": [],
+    "comm.cu": [],
     "compile_pool.cpp": [],
 }
 
@@ -47,7 +49,8 @@ def _run(cmd: list) -> None:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".h")] + \
+        [os.path.join(INCLUDE, f) for f in os.listdir(INCLUDE) if f.endswith(".h")]
     objs = []
     for src, extra in SOURCES.items():
         path = os.path.join(CSRC, src)
@@ -57,7 +60,7 @@ def build(verbose: bool = False) -> str:
         objs.append(obj)
         if _stale(obj, [path] + headers + [__file__]):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-I", CSRC, "-I", os.path.join(CUDA, "include"), *extra, "-c", path, "-o", obj]
+                   "-I", CSRC, "-I", INCLUDE, "-I", os.path.join(CUDA, "include"), *extra, "-c", path, "-o", obj]
             if src.endswith(".cpp"):
                 cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", CSRC, *extra, "-c", path, "-o", obj]
             if verbose:

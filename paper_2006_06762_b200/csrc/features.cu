@@ -446,9 +446,93 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
 // thread kernel uses (same operand order, --fmad=false), so rows are identical.
 // A block of FW_WARPS warps stages FW_CHUNK rows in shared memory and writes
 // them out coalesced (column-major: FW_CHUNK consecutive statements per column).
-constexpr int FW_WARPS = 8;
-constexpr int FW_CHUNK = 32;
+constexpr int FW_WARPS = 4;
+constexpr int FW_CHUNK = 16;
 constexpr int FW_LD = NF + 1;            // odd row stride: conflict-free lane-per-column access
+
+// Decode-AST evaluation for the warp kernel: same operations as ast_interval /
+// ast_eval, with the top three stack entries in registers (the decode ASTs of
+// real States need depth <= 4; deeper entries go to a small local array).
+struct RegStack {
+  Iv a, b, c;          // a = top
+  Iv deep[MAX_STACK];
+  int sp;
+  __device__ __forceinline__ void push(Iv v) {
+    if (sp >= 3) deep[sp - 3] = c;
+    c = b; b = a; a = v; ++sp;
+  }
+  __device__ __forceinline__ Iv pop() {
+    Iv v = a;
+    a = b; b = c;
+    if (sp > 3) c = deep[sp - 4];
+    --sp;
+    return v;
+  }
+};
+
+__device__ __forceinline__ bool ast_interval_w(const int32_t* nodes, int cnt, const int32_t* loops, int pos,
+                                               Iv& out) {
+  RegStack st;
+  st.sp = 0;
+  for (int n = 0; n < cnt; ++n) {
+    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
+    if (op == 0) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{0, loop_hi(loops, arg, pos)});
+    } else if (op == 1) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{arg, arg});
+    } else if (op == 2) {
+      if (st.sp < 2) return false;
+      Iv b = st.pop();
+      st.a.lo += b.lo; st.a.hi += b.hi;
+    } else {
+      if (st.sp < 1) return false;
+      Iv a = st.a;
+      const long long c = arg;
+      if (op == 3) st.a = c >= 0 ? Iv{a.lo * c, a.hi * c} : Iv{a.hi * c, a.lo * c};
+      else if (op == 4) st.a = Iv{fdiv(a.lo, c), fdiv(a.hi, c)};
+      else if (op == 5) {
+        if (fdiv(a.lo, c) == fdiv(a.hi, c)) st.a = Iv{fmod_(a.lo, c), fmod_(a.hi, c)};
+        else st.a = Iv{0, c - 1};
+      } else return false;
+    }
+  }
+  if (st.sp != 1) return false;
+  out = st.a;
+  return true;
+}
+
+__device__ __forceinline__ bool ast_eval_w(const int32_t* nodes, int cnt, int one_at, long long& out) {
+  RegStack st;        // lo carries the value
+  st.sp = 0;
+  for (int n = 0; n < cnt; ++n) {
+    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
+    if (op == 0) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{(arg == one_at) ? 1 : 0, 0});
+    } else if (op == 1) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{arg, 0});
+    } else if (op == 2) {
+      if (st.sp < 2) return false;
+      Iv b = st.pop();
+      st.a.lo += b.lo;
+    } else {
+      if (st.sp < 1) return false;
+      if (op == 3) st.a.lo *= arg;
+      else if (op == 4) st.a.lo = fdiv(st.a.lo, arg);
+      else if (op == 5) st.a.lo = fmod_(st.a.lo, arg);
+      else return false;
+    }
+  }
+  if (st.sp != 1) return false;
+  out = st.a.lo;
+  return true;
+}
+
+constexpr int FW_REC = 768;        // statement record words staged in shared memory (longest seen: 635)
+constexpr int FW_TAB = 192;        // memoised (position, iterator) intervals (largest seen: 14 x 8)
 
 struct WarpScratch {
   unsigned long long iter_mask[MAX_ITERS];
@@ -460,14 +544,17 @@ struct WarpScratch {
       strd[MAX_VIEWS];
   int acc[MAX_VIEWS], reuse[MAX_VIEWS];
   double ws[MAX_NEST];
+  unsigned long long inside[MAX_NEST];
   int ok;
+  Iv tab[FW_TAB];                  // interval of iterator it at position pos: tab[pos * n_iter + it]
+  int32_t rec[FW_REC];
 };
 
 // interval of iterator `it` at nest position pos (pos < 0: own ranges)
 __device__ __forceinline__ Iv iter_interval(const int32_t* nodes, const int32_t* itab, const int32_t* loops, int it,
                                             int pos, bool& ok) {
   Iv r{0, 0};
-  ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, r);
+  ok &= ast_interval_w(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, r);
   return r;
 }
 
@@ -479,6 +566,14 @@ __device__ void warp_feature_row(const int32_t* __restrict__ words, const int64_
                                  double* __restrict__ row, WarpScratch& S, int* __restrict__ err) {
   const int lane = threadIdx.x & 31;
   const int32_t* r = words + stmt_off[s];
+  {
+    const int64_t len = stmt_off[s + 1] - stmt_off[s];
+    if (len <= FW_REC) {                 // the record in shared memory: every later read is on-chip
+      for (int i = lane; i < len; i += 32) S.rec[i] = r[i];
+      __syncwarp();
+      r = S.rec;
+    }
+  }
   const int n_nest = r[0], own_start = r[1], n_loops = r[2], n_iter = r[3], n_views = r[4];
   const int unroll = r[5], n_live = r[6], has_reduce = r[7] & 1, gpu_feats = r[7] & 2;
   const int32_t* ops = r + 8;
@@ -506,8 +601,8 @@ __device__ void warp_feature_row(const int32_t* __restrict__ words, const int64_
     S.iv[it] = iter_interval(nodes, itab, loops, it, -1, ok);
     if (inner_own >= 0) {
       long long v0 = 0, v1 = 0;
-      ok &= ast_eval(nd, itab[2 * it + 1], -1, v0);
-      ok &= ast_eval(nd, itab[2 * it + 1], inner_own, v1);
+      ok &= ast_eval_w(nd, itab[2 * it + 1], -1, v0);
+      ok &= ast_eval_w(nd, itab[2 * it + 1], inner_own, v1);
       S.val0[it] = v0;
       S.val1[it] = v1;
     }
@@ -604,31 +699,61 @@ __device__ void warp_feature_row(const int32_t* __restrict__ words, const int64_
     }
     S.strd[v] = sv;
   }
-  // ---- lane per nest position: working set inside it (src/features.py:266-274)
+  // ---- working set inside each nest position (src/features.py:266-274).  An
+  // iterator's interval at position pos depends only on which of ITS own loops
+  // sit inside pos; lane = iterator walks the positions and re-evaluates only
+  // when that set changes (memoised into S.tab), then lane = position sums the
+  // views' hull products from the table.
+  for (int pos = lane; pos < n_nest; pos += 32) {
+    unsigned long long in = 0;
+    for (int j = 0; j < n_loops; ++j)
+      if (loops[3 * j + 2] > pos) in |= 1ULL << j;
+    S.inside[pos] = in;
+  }
+  __syncwarp();
+  const bool memo = n_nest * n_iter <= FW_TAB;
+  if (memo && lane < n_iter) {
+    const int it = lane;
+    unsigned long long seen = 0;
+    Iv cur{0, 0};
+    for (int pos = 0; pos < n_nest; ++pos) {
+      const unsigned long long key = S.iter_mask[it] & S.inside[pos];
+      if (pos == 0 || key != seen) {
+        cur = iter_interval(nodes, itab, loops, it, pos, ok);
+        seen = key;
+      }
+      S.tab[pos * n_iter + it] = cur;
+    }
+  }
+  __syncwarp();
   for (int pos = lane; pos < n_nest; pos += 32) {
     double acc_ws = 0.0;
     for (int v = 0; v < n_views; ++v) {
       long long pr = 1;
       const int32_t* d = r + S.vdims[v];
       for (int k = 0; k < S.vndims[v]; ++k) {
-        long long lo = d[3], hi = d[3];
-        for (int t = 0; t < d[4]; ++t) {
-          const Iv a = iter_interval(nodes, itab, loops, d[5 + 2 * t], pos, ok);
-          long long c = d[6 + 2 * t];
-          if (c >= 0) { lo += c * a.lo; hi += c * a.hi; }
-          else { lo += c * a.hi; hi += c * a.lo; }
+        if (memo) {
+          pr *= hull_width(d, S.tab + pos * n_iter);
+        } else {
+          long long lo = d[3], hi = d[3];
+          for (int t = 0; t < d[4]; ++t) {
+            const Iv a = iter_interval(nodes, itab, loops, d[5 + 2 * t], pos, ok);
+            long long c = d[6 + 2 * t];
+            if (c >= 0) { lo += c * a.lo; hi += c * a.hi; }
+            else { lo += c * a.hi; hi += c * a.lo; }
+          }
+          int st = d[1], pext = d[2];
+          if (pext > 0) {
+            if (st > 1) { lo = fdiv(lo, st); hi = fdiv(hi, st); }
+            if (fdiv(lo, pext) == fdiv(hi, pext)) { lo = fmod_(lo, pext); hi = fmod_(hi, pext); }
+            else { lo = 0; hi = pext - 1; }
+          }
+          long long size = d[0];
+          long long l2 = lo > 0 ? lo : 0;
+          long long h2 = hi < size - 1 ? hi : size - 1;
+          long long w = h2 - l2 + 1;
+          pr *= (w > 1 ? w : 1);
         }
-        int st = d[1], pext = d[2];
-        if (pext > 0) {
-          if (st > 1) { lo = fdiv(lo, st); hi = fdiv(hi, st); }
-          if (fdiv(lo, pext) == fdiv(hi, pext)) { lo = fmod_(lo, pext); hi = fmod_(hi, pext); }
-          else { lo = 0; hi = pext - 1; }
-        }
-        long long size = d[0];
-        long long l2 = lo > 0 ? lo : 0;
-        long long h2 = hi < size - 1 ? hi : size - 1;
-        long long w = h2 - l2 + 1;
-        pr *= (w > 1 ? w : 1);
         d = dim_next(d);
       }
       acc_ws += (double)pr * 4.0;

@@ -56,6 +56,15 @@ _SIGS = [
     ("lt_init", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
     ("lt_shutdown", ctypes.c_int, []),
     ("lt_task_fill", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32]),
+    # multi-GPU exchange for C callers (csrc/comm.cu)
+    ("lt_comm_unique_id", ctypes.c_int, [ctypes.c_char_p]),
+    ("lt_comm_create", ctypes.c_int64, [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    ("lt_comm_destroy", None, [ctypes.c_int64]),
+    ("lt_comm_rank", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    ("lt_comm_allgather", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]),
+    ("lt_comm_allgather_records", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]),
+    ("lt_comm_allgather_f64", ctypes.c_int, [ctypes.c_int64, c_f64p, ctypes.c_int64, c_f64p]),
+    ("lt_comm_broadcast", ctypes.c_int, [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]),
     # GBDT training (csrc/gbdt.cu)
     ("lt_gbdt_create", ctypes.c_int64, [c_f64p, ctypes.c_int64, ctypes.c_int]),
     ("lt_gbdt_destroy", None, [ctypes.c_int64]),

@@ -153,3 +153,34 @@ def test_tree_per_warp_and_thread_per_row_predict_agree_bitwise(corpus, monkeypa
     monkeypatch.delenv("LT_PREDICT_THREAD_PER_ROW")
     assert np.array_equal(a, b)
     assert np.array_equal(a[:len(corpus.scores)], corpus.scores)
+
+
+def test_c_abi_comm_single_rank_roundtrip():
+    """The C-ABI multi-GPU exchange (csrc/comm.cu, NCCL) on a one-rank
+    communicator: all-gather and broadcast are the identity."""
+    import ctypes
+    from paper_2006_06762_b200 import runtime as rt
+    lib = rt.load()
+    uid = ctypes.create_string_buffer(128)
+    rt.check(lib.lt_comm_unique_id(uid), "unique id")
+    comm = lib.lt_comm_create(uid.raw, 0, 1, 0)
+    assert comm, lib.lt_last_error().decode()
+    try:
+        rank, world = ctypes.c_int(), ctypes.c_int()
+        rt.check(lib.lt_comm_rank(comm, ctypes.byref(rank), ctypes.byref(world)), "rank")
+        assert (rank.value, world.value) == (0, 1)
+        fit = np.arange(37, dtype=np.float64) * 0.5
+        out = np.zeros_like(fit)
+        rt.check(lib.lt_comm_allgather_f64(comm, rt.ptr(fit, rt.c_f64p), len(fit), rt.ptr(out, rt.c_f64p)), "gather")
+        assert np.array_equal(out, fit)
+        recs = (rt.MeasureRecord * 3)()
+        for i in range(3):
+            recs[i].cost_us, recs[i].status = 10.0 + i, i % 2
+        got = (rt.MeasureRecord * 3)()
+        rt.check(lib.lt_comm_allgather_records(comm, ctypes.addressof(recs), 3, ctypes.addressof(got)), "records")
+        assert [(r.cost_us, r.status) for r in got] == [(10.0, 0), (11.0, 1), (12.0, 0)]
+        blob = np.frombuffer(b"model-json" * 100, dtype=np.uint8).copy()
+        rt.check(lib.lt_comm_broadcast(comm, blob.ctypes.data, blob.nbytes, 0), "broadcast")
+        assert blob.tobytes() == b"model-json" * 100
+    finally:
+        lib.lt_comm_destroy(comm)
