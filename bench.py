@@ -15,8 +15,9 @@ Metric (both arms, identical string): "measured candidates/sec (<CFG>, SSSRRSRS)
   the region (CUDA events, synchronize + barrier on both sides, max over ranks)
   contains the whole host pipeline.  `e2e`: the same States again through the
   public `measure_batch` from scratch — a fresh measuring process (new CUDA
-  context, empty cubin cache) and, every step, the DAG's inputs copied from
-  pinned host memory and the fp64 ground truth recomputed, results read back.
+  context, empty cubin cache, its own untimed warm-up steps) and, every timed
+  step, the DAG's inputs copied from host memory and the fp64 ground truth
+  recomputed, results read back.
 * `--impl reference`: the reference's own runner (`loomtune.machine.measure_batch`,
   src/machine.py:249-285, imported unchanged from baseline/_ref) on the same
   timed States, one State per task on a process pool over all host cores (a work
@@ -496,6 +497,7 @@ def main() -> None:
     runner = measure.configure(device=local, workers=workers, cache_dir=tempfile.mkdtemp(prefix="lt_cubin_e2e_"),
                                lower_workers=lower_workers)
     runner.prepare(dag, 0)
+    run_steps(dag, stream, 0, args.warmup, True)            # warm-up: the same untimed steps as above
     io_e0 = dict(runner.io)
     e2e_ms, _, _ = run_steps(dag, stream, args.warmup, args.steps, True)
     io_e1 = dict(runner.io)
@@ -584,9 +586,10 @@ def main() -> None:
             "roofline_stream_best": roofline(head),
             "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
                     "d2h_bytes_per_step": int(d2h_step), "ms_per_step": e2e_ms / args.steps,
-                    "note": "measure_batch from a fresh measuring process (new CUDA context, empty cubin cache); "
-                            "every step re-uploads the DAG's inputs (fp32 + fp64) and recomputes the fp64 ground "
-                            "truth; cubins and launch lists H2D; per-candidate error words D2H"},
+                    "note": "measure_batch from a fresh measuring process (new CUDA context, empty cubin cache, "
+                            "its own warm-up steps); every timed step re-uploads the DAG's inputs (fp32 + fp64) and "
+                            "recomputes the fp64 ground truth; cubins and launch lists H2D; per-candidate error "
+                            "words D2H"},
             "gpu_launches": n_launch,
             "clocks": clk.summary(),
             "faults": {"device_faults": stats.get("device_faults", 0), "restarts": stats.get("restarts", 0)},

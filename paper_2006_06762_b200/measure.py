@@ -92,6 +92,7 @@ class Record:
     info: dict = field(default_factory=dict)
     key: str = ""             # sha1 of the candidate's generated source
     done: bool = False        # final (False: not reached before a fault ended the batch)
+    t: dict = field(default_factory=dict)   # batch timeline (s from the batch start): lowered, start, end
 
 
 def random_inputs(dag, seed: int) -> dict:
@@ -439,6 +440,7 @@ class RunnerCore:
         """Validate + lower on this thread while a measurement thread drains
         finished compiles onto the GPU (ctypes drops the GIL inside lt_measure)."""
         t_start = time.perf_counter()
+        self._t_batch = t_start
         recs = [Record() for _ in programs]
         for p in programs:                       # device contexts are created up front
             self.context(p.dag, seed)
@@ -455,6 +457,7 @@ class RunnerCore:
                 lowered = sorted(lowered, key=lambda x: -len(x[2][1].source) if x[2][0] == "ok" else 0)
             for i, p, (kind_, payload, secs) in lowered:
                 recs[i].lower_s = secs
+                recs[i].t["lowered"] = time.perf_counter() - t_start
                 self.stats["lower_s"] += secs
                 if kind_ != "ok":
                     recs[i].detail = payload
@@ -593,7 +596,9 @@ class RunnerCore:
             print(f"[lt trace] measuring #{i} {key[:12]} {[k.info.get('template') for k in lo.kernels]}",
                   file=sys.stderr, flush=True)
         t0 = time.perf_counter()
+        rec.t["start"] = t0 - self._t_batch
         m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        rec.t["end"] = time.perf_counter() - self._t_batch
         if m.status == 2:
             # a faulting candidate is INVALID like any other failure (SPEC.md:522:
             # measure_batch never raises); the process's CUDA state is gone, so the
@@ -639,7 +644,9 @@ class RunnerCore:
             return None
         funcs = self.load(key + (":O1" if opts == PTX_SAFE_OPTS else ":O3"), data, entries)
         t0 = time.perf_counter()
+        rec.t["start"] = t0 - self._t_batch
         m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        rec.t["end"] = time.perf_counter() - self._t_batch
         if m.status == 2:
             self.faulted = True
             return None

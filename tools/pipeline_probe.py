@@ -60,6 +60,14 @@ def main() -> None:
            "best_us": min((x.cost_us for x in valid), default=None),
            "best_tflops": max((FLOPS[args.cfg] / x.cost_us / 1e6 for x in valid), default=None),
            "sum_cost_us": sum(x.cost_us for x in valid)}
+    # batch timeline: when lowering finished, when the device started / finished each candidate
+    lw = [x.t["lowered"] for x in recs if "lowered" in x.t]
+    ends = sorted((x.t["start"], x.t["end"]) for x in recs if "start" in x.t)
+    busy = sum(e - b for b, e in ends)
+    out["timeline"] = {"last_lowered": max(lw, default=None), "first_device_start": ends[0][0] if ends else None,
+                       "last_device_end": ends[-1][1] if ends else None, "device_busy": busy,
+                       "device_start_p50": pct([b for b, _ in ends], 0.5),
+                       "device_start_p90": pct([b for b, _ in ends], 0.9)}
     print(json.dumps(out), flush=True)
     if args.out:
         with open(args.out, "a") as fh:

@@ -81,7 +81,10 @@ def main() -> None:
            "best_history": importlib.import_module("loomtune.ir").history_to_json(task.best_program.history),
            "history": measured}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", f"tune_{cfg}_s{seed}{'_rules' if gpu_rules else ''}.json"), "w") as fh:
+    import gzip
+    # every measured history is kept, gzip-compressed (a 2000-trial tune is ~8 MB as JSON)
+    with gzip.open(os.path.join(ROOT, "gpurun_out", f"tune_{cfg}_s{seed}{'_rules' if gpu_rules else ''}.json.gz"),
+                   "wt") as fh:
         json.dump(out, fh)
     print(json.dumps({k: v for k, v in out.items() if k not in ("history", "best_history", "latency_curve")}))
     print("latency curve (us):", [round(x, 1) for x in task.latency])
