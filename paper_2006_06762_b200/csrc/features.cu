@@ -900,7 +900,11 @@ features_kernel(const int32_t* __restrict__ words, const int64_t* __restrict__ s
 static int launch_features(const int32_t* d_words, const int64_t* d_stmt_off, int64_t n_stmt, double* d_out,
                            int64_t ld_col, int* d_err, void* stream) {
   if (n_stmt <= 0) return 0;
-  if (getenv("LT_FEATURES_THREAD") == nullptr) {
+  // the thread-per-statement kernel is the default: the warp-per-statement kernel
+  // moves 1.02x the algorithmic DRAM bytes (vs 4.2x) but is ~9x slower (r02 ncu,
+  // profiles/r02_scoring_kernels_ncu.txt): the per-statement work is a serial
+  // chain of decode-AST interpretation that a warp cannot spread over its lanes
+  if (getenv("LT_FEATURES_WARP") != nullptr) {
     static int wsms = -1, wdev = -1;
     const size_t smem = (size_t)lt::FW_CHUNK * lt::FW_LD * sizeof(double) + lt::FW_WARPS * sizeof(lt::WarpScratch);
     int dev = 0;

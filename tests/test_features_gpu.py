@@ -129,14 +129,14 @@ def _stream_programs(n_per_cfg=256):
 
 
 def test_warp_and_thread_feature_kernels_agree_bitwise(corpus, monkeypatch):
-    """The warp-per-statement kernel (default) and the thread-per-statement
+    """The thread-per-statement kernel (default) and the warp-per-statement
     kernel compute every row identically (golden corpus + stream States)."""
     from paper_2006_06762_b200.features import extract_features_batch
     progs = list(corpus.programs) + _stream_programs()
-    warp = extract_features_batch(progs)
-    monkeypatch.setenv("LT_FEATURES_THREAD", "1")
     thread = extract_features_batch(progs)
-    monkeypatch.delenv("LT_FEATURES_THREAD")
+    monkeypatch.setenv("LT_FEATURES_WARP", "1")
+    warp = extract_features_batch(progs)
+    monkeypatch.delenv("LT_FEATURES_WARP")
     for i, (a, b) in enumerate(zip(warp, thread)):
         assert np.array_equal(a, b), i
 
