@@ -1758,9 +1758,101 @@ def _tiled(mod: _Mod, s, levels, entry: str) -> tuple:
                 ra, rb = smem_load(*la), smem_load(*lb)
                 g(f"fma.rn.{g.ft} {acc[ai]}, {ra}, {rb}, {acc[ai]};")
 
+        def pipelined(i, cv, rv):
+            """A rolled reduction loop around a fully unrolled register tile,
+            software-pipelined: the shared operands of step r+1 are loaded into a
+            second register set while step r's FMAs issue, so the tile's FMAs do
+            not wait for their own loads (with the one or two warps per scheduler
+            the tuned tilings leave, nothing else hides shared-load latency).  The
+            loop body covers two steps with the two sets alternating; every
+            accumulator still sums the steps in loop order, so results are
+            unchanged.  Returns False when the pattern or the register budget
+            does not fit (the plain rolled loop is emitted instead)."""
+            a, lv, ext, _ = loop_list[i]
+            if ext < 2 or "pipe" in _OFF:
+                return False
+            oa, ca = smem_addr(body.lhs.buffer, body.lhs.index, cv)
+            ob, cb = smem_addr(body.rhs.buffer, body.rhs.index, cv)
+            ai0 = sum(acc_coef.get(kv, 0) * val for kv, val in cv.items())
+            ext_in = [x[2] for x in loop_list[i + 1:]]
+            keys = [(x[0], x[1]) for x in loop_list[i + 1:]]
+            grid = np.indices(ext_in).reshape(len(ext_in), -1) if ext_in else np.zeros((0, 1), np.int64)
+            ais = ai0 + np.asarray([acc_coef.get(kv, 0) for kv in keys], np.int64) @ grid
+            cas = ca + np.asarray([oa["coef"].get(kv, 0) for kv in keys], np.int64) @ grid
+            cbs = cb + np.asarray([ob["coef"].get(kv, 0) for kv in keys], np.int64) @ grid
+            plan = [(int(x), int(y), int(z)) for x, y, z in zip(ais, cas, cbs)]
+            step = {"a": oa["coef"].get((a, lv), 0), "b": ob["coef"].get((a, lv), 0)}
+            ops_ = {"a": oa, "b": ob}
+            width = {}
+            for w_ in ("a", "b"):
+                vw = ops_[w_]["vec"] if g.ft == "f32" else 1
+                width[w_] = vw if vw > 1 and step[w_] % vw == 0 else 1
+            groups = {"a": sorted({c - c % width["a"] for _, c, _ in plan}),
+                      "b": sorted({c - c % width["b"] for _, _, c in plan})}
+            n_regs = sum(len(groups[w_]) * width[w_] for w_ in ("a", "b"))
+            if n_regs > 64 or n_acc + 2 * n_regs + SPILL_MARGIN > min(255, 65536 // n_threads):
+                return False
+            sets = []
+            for _ in range(2):
+                regs = {}
+                for w_ in ("a", "b"):
+                    for g0 in groups[w_]:
+                        for j in range(width[w_]):
+                            regs[(w_, g0 + j)] = g.new(g.fr)
+                sets.append(regs)
+
+            def load(regs, shift, pred):
+                bases = {w_: sbase(ops_[w_], state["rt"]) for w_ in ("a", "b")}
+                for w_ in ("a", "b"):
+                    wd = width[w_]
+                    for g0 in groups[w_]:
+                        off = (g0 + shift * step[w_]) * g.esz
+                        names = [regs[(w_, g0 + j)] for j in range(wd)]
+                        if wd > 1:
+                            g(f"{pred}ld.shared.v{wd}.{g.ft} {{{', '.join(names)}}}, [{bases[w_]}+{off}];")
+                        else:
+                            g(f"{pred}ld.shared.{g.ft} {names[0]}, [{bases[w_]}+{off}];")
+
+            def fmas(regs):
+                for ai, xa, xb in plan:
+                    g(f"fma.rn.{g.ft} {acc[ai]}, {regs[('a', xa)]}, {regs[('b', xb)]}, {acc[ai]};")
+
+            v = g.new("%r")
+            g(f"mov.s32 {v}, 0;")
+            rv2 = {**rv, (a, lv): v}
+            saved = (state["rv"], state["rt"])
+            state["rv"], state["rt"] = rv2, tuple(sorted(rv2.items())) + thread_items
+            g.push()
+            load(sets[0], 0, "")                           # step 0
+            g.pop()
+            lab = g.new_label()
+            g.label(lab)
+            g(".pragma \"nounroll\";")
+            g.push()
+            load(sets[1], 1, "")                           # step v + 1
+            fmas(sets[0])                                  # step v
+            p2 = g.new("%p")
+            t2 = g.new("%r")
+            g(f"add.s32 {t2}, {v}, 2;")
+            g(f"setp.lt.s32 {p2}, {t2}, {ext};")
+            load(sets[0], 2, f"@{p2} ")                    # step v + 2 (when it exists)
+            fmas(sets[1])                                  # step v + 1
+            g.pop()
+            pq = g.new("%p")
+            g(f"add.s32 {v}, {v}, 2;")
+            g(f"setp.lt.s32 {pq}, {v}, {ext - 1};")
+            g(f"@{pq} bra {lab};")
+            if ext % 2:
+                fmas(sets[0])                              # the last (odd) step
+            state["rv"], state["rt"] = saved
+            return True
+
         def rec(i, cv, rv):
             if acc_in_regs and fma_reads and all(unroll[i:]):
                 region(i, cv)
+                return
+            if (acc_in_regs and fma_reads and i < len(loop_list) and not unroll[i] and all(unroll[i + 1:])
+                    and loop_list[i][1][0] == "R" and pipelined(i, cv, rv)):
                 return
             if i == len(loop_list):
                 if acc_in_regs:

@@ -64,7 +64,7 @@ def main() -> None:
             v = float(r[rix[m]].replace(",", ""))
             u = units[rix[m]]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1, "usecond": 1,
-                     "nsecond": 1e-3, "msecond": 1e3}.get(u, 1)
+                     "nsecond": 1e-3, "msecond": 1e3, "ms": 1e3, "s": 1e6, "second": 1e6}.get(u, 1)
             return v * scale
         kernels[name] = {"dram_read_bytes": val("dram__bytes_read.sum"),
                          "dram_write_bytes": val("dram__bytes_write.sum"),
