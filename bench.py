@@ -68,6 +68,18 @@ def load_stream(cfg: str):
     return ComputeDAG.from_json(data["dag"]), [history_from_json(h) for h in data["histories"]]
 
 
+def bounded_batch(args, n_states: int, world: int) -> int:
+    """Candidates per rank per step: --batch, unless the stream is too short for
+    every timed candidate to be a fresh State (then the largest batch it allows);
+    both arms use the same value, hence the same States."""
+    if (args.warmup + args.steps) * args.batch * world <= n_states:
+        return args.batch
+    b = n_states // ((args.warmup + args.steps) * world)
+    if b < 1:
+        raise SystemExit(f"stream has {n_states} States, too few for {world} ranks")
+    return b
+
+
 def step_slice(stream: list, step: int, batch: int, world: int) -> list:
     lo = step * batch * world
     return stream[lo:lo + batch * world]
@@ -364,6 +376,7 @@ def traffic_of(sha1: str):
 def run_reference(args, cores: int) -> None:
     dag, stream = load_stream(args.config)
     world = args.gpus
+    args.batch = bounded_batch(args, len(stream), world)
     timed = [h for s in range(args.warmup, args.warmup + args.steps)
              for h in step_slice(stream, s, args.batch, world)]
     pool = RefPool(cores)
@@ -395,7 +408,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="RC", choices=sorted(FLOPS))
-    ap.add_argument("--batch", type=int, default=64, help="candidates per rank per step")
+    ap.add_argument("--batch", type=int, default=128, help="candidates per rank per step")
     ap.add_argument("--cpu-seconds", type=float, default=30.0,
                     help="cap on one reference candidate's CPU time (capped ones count as measured)")
     ap.add_argument("--sub-configs", default="G10,CL", help="extra configs measured in the same run ('' = none)")
@@ -438,9 +451,10 @@ def main() -> None:
         if world > 1:
             dist.barrier()
 
-    def run_steps(dag, stream, first: int, n: int, e2e: bool) -> tuple:
+    def run_steps(dag, stream, first: int, n: int, e2e: bool, batch: int = 0) -> tuple:
         """Time n steps with CUDA events on the current stream; max over ranks."""
-        progs = [[replay(dag, h) for h in step_slice(stream, first + s, args.batch, world)] for s in range(n)]
+        batch = batch or args.batch
+        progs = [[replay(dag, h) for h in step_slice(stream, first + s, batch, world)] for s in range(n)]
         results, records = [], []
         sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -472,9 +486,8 @@ def main() -> None:
 
     # ---- headline config --------------------------------------------------------------
     dag, stream = load_stream(args.config)
+    args.batch = bounded_batch(args, len(stream), world)
     need = (args.warmup + args.steps) * args.batch * world
-    if need > len(stream):
-        raise SystemExit(f"stream has {len(stream)} States, run needs {need}")
     runner.prepare(dag, 0)                                   # inputs + fp64 ground truth resident
     run_steps(dag, stream, 0, args.warmup, False)           # warm-up: compile workers, clocks, lowering pool
     for k in list(runner.stats):
@@ -510,10 +523,12 @@ def main() -> None:
     for cfg in [c for c in args.sub_configs.split(",") if c and c != args.config]:
         sdag, sstream = load_stream(cfg)
         runner.prepare(sdag, 0)
-        run_steps(sdag, sstream, 0, 1, False)
-        sms, sres, srec = run_steps(sdag, sstream, 1, args.sub_steps, False)
+        sb = min(args.batch, len(sstream) // ((1 + args.sub_steps) * world))     # the stream bounds the batch
+        run_steps(sdag, sstream, 0, 1, False, sb)
+        sms, sres, srec = run_steps(sdag, sstream, 1, args.sub_steps, False, sb)
         subs[cfg] = summarise(cfg, sms, sres, srec, args.sub_steps)
-        subs[cfg]["stream_states"] = [args.batch * world, (1 + args.sub_steps) * args.batch * world]
+        subs[cfg]["stream_states"] = [sb * world, (1 + args.sub_steps) * sb * world]
+        subs[cfg]["batch"] = sb
 
     # ---- best-found program per operator (north_star: >= 60% of FP32 peak) -------------
     # measured live here, through the same runner: cost = mean of CUDA-event repeats
@@ -595,7 +610,8 @@ def main() -> None:
             "faults": {"device_faults": stats.get("device_faults", 0), "restarts": stats.get("restarts", 0)},
         }
         line["configs"] = {c: {"metric": metric(c), "value": s["value"], "unit": "cand/s",
-                               "steps": args.sub_steps, "measured": s["measured"], "valid": s["valid"],
+                               "steps": args.sub_steps, "candidates_per_rank_per_step": s["batch"],
+                               "measured": s["measured"], "valid": s["valid"],
                                "best_program": {"us": s["best_us"], "tflops": s["achieved"], "flop": FLOPS[c],
                                                 "source_sha1": s["best_sha1"]},
                                "roofline": found_roofline(c) or roofline(s),
@@ -651,7 +667,7 @@ def main() -> None:
                               "CostModel.predict (tests/golden/model.json, 30 trees), chunks of 16 per process"}
                 for c in subs:
                     sdag, sstream = load_stream(c)
-                    r = ref_measure_rate(pool, sdag, step_slice(sstream, 1, args.batch, world)[:cores],
+                    r = ref_measure_rate(pool, sdag, step_slice(sstream, 1, subs[c]["batch"], world)[:cores],
                                          args.cpu_seconds)
                     line["configs"][c]["cpu_baseline"] = {
                         "value": r["value"], "unit": "cand/s", "cores": cores, "kind": "reference",

@@ -264,6 +264,43 @@ class Expr:
             a = a + self.iv(n).scale(c)
         return a
 
+    def pred(self, e):
+        """Predicate register of a condition built from comparisons of IterVal
+        with constants, multiplied together (the padding stage's in-bounds test,
+        `src/workloads.py:45-67`), in integer arithmetic: the same truth value as
+        the float evaluation (0/1 products, != 0) without int->float conversions
+        and float multiplies.  None when the condition has another shape."""
+        g = self.g
+        k = kind(e)
+        if k != "Bin":
+            return None
+        if e.op == "mul":
+            a = self.pred(e.lhs)
+            b = self.pred(e.rhs) if a is not None else None
+            if b is None:
+                return None
+            p = g.new("%p")
+            g(f"and.pred {p}, {a}, {b};")
+            return p
+        if e.op not in ("ge", "gt", "le", "lt") or "ipred" in _OFF:
+            return None
+        lhs, rhs, op = e.lhs, e.rhs, e.op
+        if kind(lhs) == "Const" and kind(rhs) == "IterVal":
+            lhs, rhs, op = rhs, lhs, {"ge": "le", "le": "ge", "gt": "lt", "lt": "gt"}[op]
+        if kind(lhs) != "IterVal" or kind(rhs) != "Const":
+            return None
+        c = float(rhs.value)
+        if not math.isfinite(c) or abs(c) > 2 ** 30:
+            return None
+        ci = math.ceil(c) if op in ("ge", "lt") else math.floor(c)   # integer x vs real c
+        a = self.lin(lhs.lin)
+        if not a.terms:
+            return None
+        x = g.aff(Aff(a.terms))
+        p = g.new("%p")
+        g(f"setp.{op}.s32 {p}, {x}, {ci - a.const};")
+        return p
+
     def __call__(self, e) -> str:
         g = self.g
         k = kind(e)
@@ -302,9 +339,11 @@ class Expr:
                 raise Unsupported(f"math call {e.fn}")
             return f
         if k == "Select":
-            c = self(e.cond)
-            p = g.new("%p")
-            g(f"setp.ne.{g.ft} {p}, {c}, {g.fconst(0.0)};")
+            p = self.pred(e.cond)
+            if p is None:
+                c = self(e.cond)
+                p = g.new("%p")
+                g(f"setp.ne.{g.ft} {p}, {c}, {g.fconst(0.0)};")
             np_ = g.new("%p")
             g(f"not.pred {np_}, {p};")
             outer = self.guard
@@ -544,9 +583,11 @@ class _Kern:
         s = self.m.live[name]
         env = {n: a for (n, _), a in zip(s.space, idx)}
         ex = Expr(g, lambda n: env[n], None)
-        c = ex(s.expr.cond)
-        p = g.new("%p")
-        g(f"setp.ne.{g.ft} {p}, {c}, {g.fconst(0.0)};")
+        p = ex.pred(s.expr.cond)
+        if p is None:
+            c = ex(s.expr.cond)
+            p = g.new("%p")
+            g(f"setp.ne.{g.ft} {p}, {c}, {g.fconst(0.0)};")
         rd = s.expr.then
         base, flat = self.gsource(rd.buffer, [ex.lin(l) for l in rd.index])
         rb, imm = g.gaddr(base, flat)

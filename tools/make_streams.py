@@ -37,7 +37,7 @@ from paper_2006_06762_b200.state import workloads as W  # noqa: E402
 OUT = os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "streams")
 
 
-def stream(cfg: str, n: int, max_draws: int = 250000) -> dict:
+def stream(cfg: str, n: int, max_draws: int = int(os.environ.get("LT_MAX_DRAWS", "250000"))) -> dict:
     name, kw = W.CONFIGS[cfg]
     ours = W.build(name, **kw)
     ref = LT.ComputeDAG.from_json(ours.to_json())
