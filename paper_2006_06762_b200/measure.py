@@ -316,6 +316,7 @@ class RunnerCore:
                               else int(os.environ.get("LT_LOWER_WORKERS", max(1, min(8, (os.cpu_count() or 2) // 2)))))
         self._lpool = None
         self.faulted = False            # a candidate faulted: this process's CUDA state is lost
+        self.force_recompile = False    # test hook: treat every first verification as failed
 
     def _lower_pool(self):
         main = sys.modules.get("__main__")
@@ -615,6 +616,8 @@ class RunnerCore:
         if m.status != 0:
             rec.detail = "gpu: " + m.detail.decode(errors="replace")
             return
+        if self.force_recompile and lo.source.startswith(".version"):
+            rec.max_rel_err = math.inf                      # test hook: exercise the recompile path
         if not (rec.max_rel_err <= GPU_TOL) and lo.source.startswith(".version") and m.status == 0:
             o1 = lo.info.get("ptxas_opt") == "-O1"
             m2 = self._remeasure_safe(lo, key, entries, ctx, PTX_OPTS if o1 else PTX_SAFE_OPTS)
@@ -644,9 +647,7 @@ class RunnerCore:
             return None
         funcs = self.load(key + (":O1" if opts == PTX_SAFE_OPTS else ":O3"), data, entries)
         t0 = time.perf_counter()
-        rec.t["start"] = t0 - self._t_batch
         m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
-        rec.t["end"] = time.perf_counter() - self._t_batch
         if m.status == 2:
             self.faulted = True
             return None
@@ -724,6 +725,9 @@ class _Server:
 
     def set_max_modules(self, n):
         self.core.max_modules = n
+
+    def set_force_recompile(self, on):
+        self.core.force_recompile = bool(on)
 
     def inject_fault(self):
         """Test hook: run a kernel that stores to an unmapped address."""
@@ -928,6 +932,11 @@ class Runner:
 
     def inject_fault(self):
         return self._call("inject_fault")
+
+    def force_recompile(self, on: bool) -> None:
+        """Test hook: every PTX candidate's first verification counts as failed, so
+        the recompile-at-the-other-ptxas-level path runs."""
+        self._call("set_force_recompile", on)
 
 
 _RUNNER: Runner | None = None

@@ -201,3 +201,24 @@ def test_module_eviction_keeps_shared_memory_grants_valid():
     assert big
     for i, r in enumerate(recs):
         assert r.status == "valid", (i, r.detail)
+
+
+def test_recompile_path_after_failed_verification(runner):
+    """A candidate whose first verification fails is recompiled at the other ptxas
+    level and measured again (measure.RunnerCore._remeasure_safe); the test hook
+    makes every first verification fail, so the path runs for every candidate."""
+    import bench
+    from paper_2006_06762_b200.state import replay
+    dag, stream = bench.load_stream("G5")
+    progs = [replay(dag, h) for h in stream[3:11]]
+    before = runner.stats.get("recompiled", 0)
+    runner.force_recompile(True)
+    try:
+        recs = runner.measure_programs(progs)
+    finally:
+        runner.force_recompile(False)
+    assert runner.stats.get("recompiled", 0) > before
+    for r in recs:
+        if r.key:                                   # lowered to a PTX candidate
+            assert r.status == "valid", r.detail
+            assert "ptxas" in r.info and r.max_rel_err <= 1e-4
