@@ -108,6 +108,9 @@ def _f64(x) -> str:
     return "0d%016X" % struct.unpack("<Q", struct.pack("<d", float(x)))[0]
 
 
+_MISSING = object()
+
+
 class Ptx:
     """One kernel's instruction stream with scoped value numbering."""
 
@@ -117,7 +120,8 @@ class Ptx:
         self.esz = 4 if self.ft == "f32" else 8
         self.n = {"%r": 0, "%rd": 0, "%p": 0, self.fr: 0}
         self.lines: list = []
-        self.scopes: list = [{}]
+        self.table: dict = {}           # key -> value, innermost scope wins
+        self.undo: list = [[]]          # per scope: (key, shadowed value) to restore on pop
         self.labels = 0
 
     def new(self, cls: str) -> str:
@@ -139,20 +143,22 @@ class Ptx:
 
     # value numbering
     def cached(self, key):
-        for sc in reversed(self.scopes):
-            if key in sc:
-                return sc[key]
-        return None
+        return self.table.get(key)
 
     def remember(self, key, val):
-        self.scopes[-1][key] = val
+        self.undo[-1].append((key, self.table.get(key, _MISSING)))
+        self.table[key] = val
         return val
 
     def push(self):
-        self.scopes.append({})
+        self.undo.append([])
 
     def pop(self):
-        self.scopes.pop()
+        for key, old in reversed(self.undo.pop()):
+            if old is _MISSING:
+                del self.table[key]
+            else:
+                self.table[key] = old
 
     # integer arithmetic
     def aff(self, a: Aff) -> str:
