@@ -137,6 +137,9 @@ int lt_task_slot(int64_t task, int slot, int64_t bytes);
 int64_t lt_task_slot_ptr(int64_t task, int slot);
 int lt_task_upload(int64_t task, int slot, const void* host, int64_t bytes);
 int lt_task_download(int64_t task, int slot, void* host, int64_t bytes);
+/* page-lock / release a host buffer that is uploaded repeatedly (the DAG's inputs) */
+int lt_host_register(void* host, int64_t bytes);
+int lt_host_unregister(void* host);
 /* fill n 32-bit words of a slot with `value`, stream-ordered (NaN-poisoning scratch) */
 int lt_task_fill(int64_t task, int slot, int64_t n, uint32_t value);
 int lt_task_run(int64_t task, const lt_launch* launches, int n);

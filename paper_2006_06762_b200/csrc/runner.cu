@@ -280,6 +280,17 @@ int lt_task_upload(int64_t handle, int slot, const void* host, int64_t bytes) {
   return lt::check_cuda(cudaStreamSynchronize(t->stream), "upload sync");
 }
 
+// Page-lock a host buffer (the DAG's inputs), so uploads from it are DMA from
+// pinned memory; unregister before freeing it.
+int lt_host_register(void* host, int64_t bytes) {
+  if (bytes <= 0) return 0;
+  return lt::check_cuda(cudaHostRegister(host, (size_t)bytes, cudaHostRegisterPortable), "cudaHostRegister");
+}
+
+int lt_host_unregister(void* host) {
+  return lt::check_cuda(cudaHostUnregister(host), "cudaHostUnregister");
+}
+
 int lt_task_download(int64_t handle, int slot, void* host, int64_t bytes) {
   Task* t = (Task*)(intptr_t)handle;
   TASK_SCOPE(t);
