@@ -45,11 +45,16 @@ def states():
 
 
 def main():
+    """Optional argument: the index of one candidate (run one per process so a
+    slow tool pass can be bounded per candidate with `timeout`)."""
     from paper_2006_06762_b200 import measure
     from paper_2006_06762_b200.ptxgen import lower_ptx
     r = measure.configure(device=0, cache_dir="", min_ms=0.0, max_repeat=1, workers=8)
     bad = 0
-    for label, p in states():
+    chosen = states()
+    if len(sys.argv) > 1:
+        chosen = [chosen[int(sys.argv[1])]]
+    for label, p in chosen:
         (rec,) = r.measure_programs([p])
         kinds = [k.info.get("template") for k in lower_ptx(p).kernels]
         print(f"{label}: {rec.status} {kinds} max_rel_err={rec.max_rel_err:.2e} {rec.detail}", flush=True)
