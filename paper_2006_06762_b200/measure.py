@@ -25,6 +25,10 @@ from __future__ import annotations
 
 import atexit
 import ctypes
+# imported before `atexit.register(_shutdown)` below: multiprocessing registers its
+# own exit hook (joining non-daemon children) at import, and atexit runs hooks in
+# reverse order, so the measuring process is told to close before it is joined
+import multiprocessing.util  # noqa: F401
 import hashlib
 import queue
 import threading

@@ -222,3 +222,29 @@ def test_recompile_path_after_failed_verification(runner):
         if r.key:                                   # lowered to a PTX candidate
             assert r.status == "valid", r.detail
             assert "ptxas" in r.info and r.max_rel_err <= 1e-4
+
+
+def test_batch_edge_cases(runner):
+    """Empty batch; a State repeated in one batch (its kernels compile once);
+    States of two different DAGs and an invalid State mixed in one batch —
+    results in input order, statuses per State (src/machine.py:249-285)."""
+    import bench
+    from paper_2006_06762_b200.measure import INVALID, VALID, measure_batch
+    from paper_2006_06762_b200.state import ComputeDAG, history_from_json, replay
+    assert measure_batch([]) == []
+    dag5, s5 = bench.load_stream("G5")
+    dagt, st = bench.load_stream("TBG")
+    p = replay(dag5, s5[7])
+    q = replay(dagt, st[20])
+    with open(os.path.join(GOLDEN, "measure.json")) as fh:
+        case = json.load(fh)[0]                        # golden case 0, State 6: two parallel loops
+    with open(os.path.join(GOLDEN, "corpus.json")) as fh:
+        gdag = ComputeDAG.from_json(json.load(fh)["dags"][case["dag"]])
+    bad = replay(gdag, history_from_json(case["histories"][6]))
+    assert case["validate"][6]
+    res = measure_batch([p, q, p, bad, q])
+    assert [r.status for r in res] == [VALID, VALID, VALID, INVALID, VALID], res
+    assert res[3].cost == math.inf and res[3].throughput == 0.0 and res[3].detail == case["validate"][6][0]
+    best = min(r.cost for r in res if r.status == VALID)
+    assert max(r.throughput for r in res) == 1.0 and all(
+        r.throughput == best / r.cost for r in res if r.status == VALID)
