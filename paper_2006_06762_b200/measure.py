@@ -10,7 +10,9 @@ ground truth on the device (max relative error <= `GPU_TOL`, the north star's
 
 Timing: one warm-up run (also verified), then, if it was shorter than
 `min_ms` (1 ms), timed repeats until the timed region spans `min_ms`; a run of
-at least `min_ms` is its own measurement.  CUDA events on the task stream.
+at least `min_ms` is its own measurement unless a kernel of the candidate uses
+local memory (spilling kernels pay for growing the local-memory pool on their
+first launch, so they always get a timed run).  CUDA events on the task stream.
 
 Statuses: INVALID (validation failure, no legal launch, compile/launch
 failure, or wrong output — detail says which), TIMEOUT (cost >=
@@ -309,7 +311,8 @@ class RunnerCore:
 
     def __init__(self, device: int = 0, workers: int | None = None, cache_dir: str | None = None,
                  min_ms: float = 1.0, max_repeat: int = 50, compile_timeout: float = 120.0,
-                 min_repeat: int = 1, backend: str = "ptx", lower_workers: int | None = None):
+                 min_repeat: int = 0, backend: str = "ptx", lower_workers: int | None = None,
+                 first_run_timing: bool = True):
         self.lib = rt.load()
         self.device = device
         rt.check(self.lib.lt_set_device(device), "set device")
@@ -320,6 +323,8 @@ class RunnerCore:
         rt.check(self.lib.lt_pool_start(self.workers, self.cache_dir.encode() if self.cache_dir else None,
                                         compile_timeout), "compile pool")
         self.min_ms, self.max_repeat, self.min_repeat = min_ms, max_repeat, min_repeat
+        self.first_run_timing = first_run_timing
+        self._local_bytes: dict = {}       # function handle -> local memory bytes per thread
         self.backend = backend
         self.ctx: dict = {}
         self._dag_keys: dict = {}          # (id(dag), seed) -> (dag, content key)
@@ -358,6 +363,7 @@ class RunnerCore:
         with self.mod_lock:
             for k in [k for k in self.modules if k not in self.pinned]:
                 self.lib.lt_module_unload(self.modules.pop(k)[0])
+            self._local_bytes.clear()
             self.failed_keys.clear()
         self.lib.lt_pool_stop()
         self.cache_dir = cache_dir
@@ -446,6 +452,7 @@ class RunnerCore:
                     break
                 old, _ = self.modules.pop(victim)
                 self.lib.lt_module_unload(old)
+                self._local_bytes.clear()       # a handle value may be handed out again
         return funcs
 
     def compile_and_load(self, sources: list, entries: list) -> list:
@@ -621,7 +628,7 @@ class RunnerCore:
                   file=sys.stderr, flush=True)
         t0 = time.perf_counter()
         rec.t["start"] = t0 - self._t_batch
-        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self.min_repeat)
+        m = ctx.measure(lo, funcs, self.min_ms, self.max_repeat, self._min_repeat(funcs))
         rec.t["end"] = time.perf_counter() - self._t_batch
         if m.status == 2:
             # a faulting candidate is INVALID like any other failure (SPEC.md:522:
@@ -659,6 +666,23 @@ class RunnerCore:
             return
         rec.status = VALID
         rec.cost_us = m.cost_us
+
+    def _min_repeat(self, funcs: list) -> int:
+        """Timed runs after the verified warm-up: a candidate whose kernels use no
+        local memory and whose warm-up run already spans `min_ms` is timed by that
+        run (0); kernels that spill keep >= 1 timed run, because their first launch
+        also pays for growing the local-memory pool (measured up to 300x)."""
+        if self.min_repeat > 0 or not self.first_run_timing:
+            return max(1, self.min_repeat)
+        for f in funcs:
+            if f not in self._local_bytes:
+                regs, local, mt, sm = (ctypes.c_int() for _ in range(4))
+                rt.check(self.lib.lt_function_info(f, ctypes.byref(regs), ctypes.byref(local), ctypes.byref(mt),
+                                                   ctypes.byref(sm)), "function info")
+                self._local_bytes[f] = local.value
+            if self._local_bytes[f]:
+                return 1
+        return 0
 
     def _remeasure_safe(self, lo, key, entries, ctx, opts):
         """Recompile a PTX candidate with the other ptxas level and measure it again

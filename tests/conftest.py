@@ -16,3 +16,11 @@ def pytest_configure(config):
 def corpus():
     from tests.golden_corpus import load_corpus
     return load_corpus()
+
+
+# LT_HANG_DUMP=1: SIGUSR1 dumps every thread's stack (diagnosing a process that
+# does not exit, e.g. `timeout -s USR1 ... pytest`)
+if os.environ.get("LT_HANG_DUMP"):
+    import faulthandler
+    import signal
+    faulthandler.register(signal.SIGUSR1, all_threads=True)
