@@ -58,30 +58,48 @@ class Aff:
     __slots__ = ("terms", "const")
 
     def __init__(self, terms=None, const=0):
-        self.terms = {r: c for r, c in (terms or {}).items() if c}
+        self.terms = {r: c for r, c in terms.items() if c} if terms else {}
         self.const = int(const)
 
     @staticmethod
+    def _raw(terms: dict, const: int) -> "Aff":
+        """No copying or zero filtering: `terms` is already clean and is never
+        mutated afterwards (Aff values are immutable; dicts may be shared)."""
+        a = object.__new__(Aff)
+        a.terms, a.const = terms, const
+        return a
+
+    @staticmethod
     def reg(r, c=1):
-        return Aff({r: c})
+        return Aff._raw({r: c} if c else {}, 0)
 
     @staticmethod
     def k(c):
-        return Aff({}, c)
+        return Aff._raw({}, int(c))
 
     def __add__(self, o):
         if isinstance(o, int):
-            return Aff(self.terms, self.const + o)
+            return Aff._raw(self.terms, self.const + o)
+        if not o.terms:
+            return Aff._raw(self.terms, self.const + o.const)
+        if not self.terms:
+            return Aff._raw(o.terms, self.const + o.const)
         t = dict(self.terms)
         for r, c in o.terms.items():
-            t[r] = t.get(r, 0) + c
-        return Aff(t, self.const + o.const)
+            v = t.get(r, 0) + c
+            if v:
+                t[r] = v
+            else:
+                del t[r]
+        return Aff._raw(t, self.const + o.const)
 
     def scale(self, s):
-        return Aff({r: c * s for r, c in self.terms.items()}, self.const * s)
+        if not s:
+            return Aff._raw({}, 0)
+        return Aff._raw({r: c * s for r, c in self.terms.items()}, self.const * s)
 
     def runtime(self):
-        return Aff(self.terms, 0)
+        return Aff._raw(self.terms, 0)
 
     def key(self):
         return tuple(sorted(self.terms.items()))
