@@ -60,23 +60,39 @@ def _ops(expr, cache: dict) -> list:
     return hit[1]
 
 
+_DECODE_OP = {"DMul": OP_MUL, "DDiv": OP_DIV, "DMod": OP_MOD}
+
+
 def _postfix(d, loop_idx: dict, out: list) -> None:
-    k = kind(d)
-    if k == "DVar":
-        if d.loop not in loop_idx:
-            raise EncodeError(f"decode references unknown loop {d.loop!r}")
-        out += (OP_VAR, loop_idx[d.loop])
-    elif k == "DConst":
-        out += (OP_CONST, int(d.value))
-    elif k == "DAdd":
-        _postfix(d.a, loop_idx, out)
-        _postfix(d.b, loop_idx, out)
-        out += (OP_ADD, 0)
-    else:
-        if d.c is None:
-            raise EncodeError("symbolic factor in decode")
-        _postfix(d.a, loop_idx, out)
-        out += ({"DMul": OP_MUL, "DDiv": OP_DIV, "DMod": OP_MOD}[k], int(d.c))
+    """Postfix form of a decode AST (`src/ir.py:36-70`), iteratively: operands
+    before operators, DAdd's left subtree first."""
+    stack = [(d, False)]
+    pop, push = stack.pop, stack.append
+    while stack:
+        node, done = pop()
+        k = type(node).__name__
+        if k == "DVar":
+            j = loop_idx.get(node.loop)
+            if j is None:
+                raise EncodeError(f"decode references unknown loop {node.loop!r}")
+            out += (OP_VAR, j)
+        elif k == "DConst":
+            out += (OP_CONST, int(node.value))
+        elif k == "DAdd":
+            if done:
+                out += (OP_ADD, 0)
+            else:
+                push((node, True))
+                push((node.b, False))
+                push((node.a, False))
+        else:
+            if done:
+                out += (_DECODE_OP[k], int(node.c))
+            else:
+                if node.c is None:
+                    raise EncodeError("symbolic factor in decode")
+                push((node, True))
+                push((node.a, False))
 
 
 def _stage_map(p) -> dict:
@@ -198,8 +214,10 @@ def encode_batch(programs, gpu_features: bool = False) -> tuple:
     cache: dict = {}
     for p in programs:
         prog_off.append(prog_off[-1] + encode_program(p, recs, cache, gpu_features))
-    lens = np.fromiter((len(r) for r in recs), dtype=np.int64, count=len(recs))
     stmt_off = np.zeros(len(recs) + 1, dtype=np.int64)
-    np.cumsum(lens, out=stmt_off[1:])
-    words = np.fromiter((w for r in recs for w in r), dtype=np.int32, count=int(stmt_off[-1]))
+    np.cumsum([len(r) for r in recs], out=stmt_off[1:])
+    flat: list = []
+    for r in recs:
+        flat.extend(r)
+    words = np.array(flat, dtype=np.int32)
     return words, stmt_off, np.asarray(prog_off, dtype=np.int64)
