@@ -23,6 +23,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <vector>
+#include <tuple>
 #include <string>
 #include "common.h"
 #include "npsum.cuh"
@@ -41,6 +42,10 @@ struct Node {
 struct Model {
   int n_trees = 0;
   int n_nodes = 0;
+  int depth = -1;              // perfect layout depth D (-1: not available)
+  double* d_pthr = nullptr;    // [n_trees][2^D - 1] thresholds
+  int32_t* d_pfeat = nullptr;  // [n_trees][2^D - 1] compact feature columns
+  double* d_pval = nullptr;    // [n_trees][2^D] leaf value*eta
   int n_used = 0;          // compact feature columns
   double base = 0.0;
   Node* d_nodes = nullptr;
@@ -134,6 +139,65 @@ predict_trees_kernel(const double* __restrict__ X, int64_t n_rows, bool col_majo
   }
 }
 
+// Perfect-tree walk: every tree padded to a complete tree of depth D (a leaf
+// above the bottom level is replicated into all bottom leaves below it, so the
+// direction taken under it does not matter, NaN included).  Each level is one
+// shared threshold load, one shared feature load and a compare: child =
+// 2*i + 1 + !(x <= thr), no per-node child indices, no data-dependent trip count
+// (the warp stays converged).  Same comparisons, leaf values and per-row
+// summation order as the other kernels: bit-identical scores.
+constexpr int MAX_PERFECT_DEPTH = 7;
+
+__global__ void __launch_bounds__(TREE_WARPS * 32)
+predict_perfect_kernel(const double* __restrict__ X, int64_t n_rows, bool col_major, const double* __restrict__ pthr,
+                       const int32_t* __restrict__ pfeat, const double* __restrict__ pval, int depth, int n_trees,
+                       const int32_t* __restrict__ used, int n_used, double base, double* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n_int = (1 << depth) - 1, n_leaf = 1 << depth;
+  double* s_thr = (double*)smem_raw;                                  // n_trees x n_int
+  double* s_val = s_thr + (size_t)n_trees * n_int;                    // n_trees x n_leaf
+  double* tile = s_val + (size_t)n_trees * n_leaf;                    // n_used x TILE_ROWS
+  double* part = tile + (size_t)n_used * TILE_ROWS;                   // n_trees x TILE_ROWS
+  int32_t* s_feat = (int32_t*)(part + (size_t)n_trees * TILE_ROWS);   // n_trees x n_int
+  for (int i = threadIdx.x; i < n_trees * n_int; i += blockDim.x) {
+    s_thr[i] = pthr[i];
+    s_feat[i] = pfeat[i] * TILE_ROWS;                                 // pre-scaled tile column offset
+  }
+  for (int i = threadIdx.x; i < n_trees * n_leaf; i += blockDim.x) s_val[i] = pval[i];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t row0 = (int64_t)blockIdx.x * TILE_ROWS; row0 < n_rows; row0 += (int64_t)gridDim.x * TILE_ROWS) {
+    const int rows_here = (int)min((int64_t)TILE_ROWS, n_rows - row0);
+    __syncthreads();
+    if (col_major) {
+      for (int e = threadIdx.x; e < n_used * TILE_ROWS; e += blockDim.x) {
+        const int c = e / TILE_ROWS, r = e - c * TILE_ROWS;
+        if (r < rows_here) tile[e] = X[(int64_t)used[c] * n_rows + row0 + r];
+      }
+    } else {
+      for (int e = threadIdx.x; e < n_used * TILE_ROWS; e += blockDim.x) {
+        const int r = e / n_used, c = e - r * n_used;
+        if (r < rows_here) tile[c * TILE_ROWS + r] = X[(row0 + r) * NF + used[c]];
+      }
+    }
+    __syncthreads();
+    for (int t = warp; t < n_trees; t += TREE_WARPS) {
+      const double* thr = s_thr + t * n_int;
+      const int32_t* feat = s_feat + t * n_int;
+      for (int r = lane; r < rows_here; r += 32) {
+        int i = 0;
+        for (int lvl = 0; lvl < depth; ++lvl) i = 2 * i + 1 + (tile[feat[i] + r] <= thr[i] ? 0 : 1);
+        part[t * TILE_ROWS + r] = s_val[t * n_leaf + (i - n_int)];
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < rows_here; r += blockDim.x) {
+      double acc = base;
+      for (int t = 0; t < n_trees; ++t) acc = __dadd_rn(acc, part[t * TILE_ROWS + r]);
+      out[row0 + r] = acc;
+    }
+  }
+}
+
 __global__ void segment_sum_kernel(const double* __restrict__ row_scores, const int64_t* __restrict__ prog_off,
                                    int64_t n_prog, double* __restrict__ out) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -187,6 +251,56 @@ int64_t lt_model_create(int n_trees, const int64_t* tree_node_off, const int32_t
   }
   toff[n_trees] = (int32_t)total;
   if (used.empty()) used.push_back(0);
+  // perfect layout (see predict_perfect_kernel) when every tree is at most 7 deep
+  int depth = 0;
+  bool perfect = true;
+  std::vector<int> level;
+  for (int t = 0; t < n_trees && perfect; ++t) {
+    int64_t o = tree_node_off[t], n = tree_node_off[t + 1] - o;
+    level.assign((size_t)n, -1);
+    level[0] = 0;
+    for (int64_t i = 0; i < n; ++i) {            // children follow their parent (breadth-first ids)
+      if (level[i] < 0) { perfect = false; break; }
+      if (feature[o + i] >= 0) {
+        for (int32_t c : {left[o + i], right[o + i]}) {
+          if (c <= i || level[c] >= 0) { perfect = false; break; }
+          level[c] = level[i] + 1;
+        }
+        if (!perfect) break;
+      } else if (level[i] > depth) {
+        depth = level[i];
+      }
+    }
+    if (depth > lt::MAX_PERFECT_DEPTH) perfect = false;
+  }
+  std::vector<double> pthr, pval;
+  std::vector<int32_t> pfeat;
+  if (perfect && n_trees > 0) {
+    const int n_int = (1 << depth) - 1, n_leaf = 1 << depth;
+    pthr.assign((size_t)n_trees * n_int, 0.0);
+    pfeat.assign((size_t)n_trees * n_int, 0);
+    pval.assign((size_t)n_trees * n_leaf, 0.0);
+    for (int t = 0; t < n_trees; ++t) {
+      const int64_t o = tree_node_off[t];
+      // (node, perfect position, level) work list
+      std::vector<std::tuple<int64_t, int, int>> work{{0, 0, 0}};
+      while (!work.empty()) {
+        auto [nd, pos, lv] = work.back();
+        work.pop_back();
+        if (feature[o + nd] >= 0) {
+          pthr[(size_t)t * n_int + pos] = nodes[o + nd].x;
+          pfeat[(size_t)t * n_int + pos] = nodes[o + nd].feat;
+          work.push_back({left[o + nd], 2 * pos + 1, lv + 1});
+          work.push_back({right[o + nd], 2 * pos + 2, lv + 1});
+        } else {
+          // replicate the leaf into every bottom position under pos
+          int first = pos, span = 1;
+          for (int k = lv; k < depth; ++k) { first = 2 * first + 1; span *= 2; }
+          for (int j = 0; j < span; ++j) pval[(size_t)t * n_leaf + (first - n_int) + j] = nodes[o + nd].x;
+        }
+      }
+    }
+  }
   Model* m = new Model();
   m->n_trees = n_trees;
   m->n_nodes = (int)nodes.size();
@@ -201,6 +315,18 @@ int64_t lt_model_create(int n_trees, const int64_t* tree_node_off, const int32_t
   cudaMemcpy(m->d_nodes, nodes.data(), nodes.size() * sizeof(Node), cudaMemcpyHostToDevice);
   cudaMemcpy(m->d_tree_off, toff.data(), toff.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
   cudaMemcpy(m->d_used, used.data(), used.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+  if (!pthr.empty()) {
+    if (lt::check_cuda(cudaMalloc(&m->d_pthr, pthr.size() * sizeof(double)), "cudaMalloc pthr") ||
+        lt::check_cuda(cudaMalloc(&m->d_pfeat, pfeat.size() * sizeof(int32_t)), "cudaMalloc pfeat") ||
+        lt::check_cuda(cudaMalloc(&m->d_pval, pval.size() * sizeof(double)), "cudaMalloc pval")) {
+      delete m;
+      return 0;
+    }
+    cudaMemcpy(m->d_pthr, pthr.data(), pthr.size() * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(m->d_pfeat, pfeat.data(), pfeat.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    cudaMemcpy(m->d_pval, pval.data(), pval.size() * sizeof(double), cudaMemcpyHostToDevice);
+    m->depth = depth;
+  }
   if (lt::check_cuda(cudaGetLastError(), "model upload")) { delete m; return 0; }
   return (int64_t)(intptr_t)m;
 }
@@ -211,6 +337,9 @@ void lt_model_destroy(int64_t handle) {
   cudaFree(m->d_nodes);
   cudaFree(m->d_tree_off);
   cudaFree(m->d_used);
+  if (m->d_pthr) cudaFree(m->d_pthr);
+  if (m->d_pfeat) cudaFree(m->d_pfeat);
+  if (m->d_pval) cudaFree(m->d_pval);
   delete m;
 }
 
@@ -247,6 +376,30 @@ static int predict_device(int64_t handle, const double* d_rows, int64_t n_rows, 
   int sms = 0;
   size_t optin = 0;
   const int tdev = device_props(&sms, &optin);
+  if (m->depth >= 0 && getenv("LT_PREDICT_IRREGULAR") == nullptr && getenv("LT_PREDICT_THREAD_PER_ROW") == nullptr) {
+    const size_t n_int = ((size_t)1 << m->depth) - 1, n_leaf = (size_t)1 << m->depth;
+    const size_t psmem = (size_t)m->n_trees * (n_int + n_leaf) * sizeof(double) +
+                         (size_t)(m->n_used + m->n_trees) * lt::TILE_ROWS * sizeof(double) +
+                         (size_t)m->n_trees * n_int * sizeof(int32_t);
+    if (psmem <= optin) {
+      static size_t pconfigured[64] = {};
+      if (psmem > 48 * 1024 && (tdev < 0 || tdev >= 64 || psmem > pconfigured[tdev])) {
+        if (lt::check_cuda(cudaFuncSetAttribute(lt::predict_perfect_kernel,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psmem),
+                           "smem attr"))
+          return -1;
+        if (tdev >= 0 && tdev < 64) pconfigured[tdev] = psmem;
+      }
+      const int per_sm = psmem <= optin / 2 ? 2 : 1;
+      int64_t tiles = (n_rows + lt::TILE_ROWS - 1) / lt::TILE_ROWS;
+      int64_t blocks = (int64_t)sms * per_sm;
+      if (blocks > tiles) blocks = tiles;
+      lt::predict_perfect_kernel<<<(unsigned)blocks, lt::TREE_WARPS * 32, psmem, (cudaStream_t)stream>>>(
+          d_rows, n_rows, col_major, m->d_pthr, m->d_pfeat, m->d_pval, m->depth, m->n_trees, m->d_used, m->n_used,
+          m->base, d_row_scores);
+      return lt::check_launch("predict_perfect_kernel");
+    }
+  }
   const size_t tsmem = (size_t)m->n_nodes * sizeof(Node) +
                        (size_t)(m->n_used + m->n_trees) * lt::TILE_ROWS * sizeof(double) +
                        (size_t)(m->n_trees + 1) * sizeof(int32_t);

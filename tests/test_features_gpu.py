@@ -142,17 +142,37 @@ def test_warp_and_thread_feature_kernels_agree_bitwise(corpus, monkeypatch):
 
 
 def test_tree_per_warp_and_thread_per_row_predict_agree_bitwise(corpus, monkeypatch):
-    """One-tree-per-warp predict (default, model in shared memory) equals the
-    thread-per-row kernel bit for bit, and both equal the golden scores."""
+    """The three predict kernels — perfect-tree walk (default), irregular
+    tree-per-warp, thread-per-row — give bit-identical scores, equal to the
+    golden scores; also for a model with early leaves, a depth-0 tree and NaN
+    features (the padded subtrees must not change the leaf)."""
     from paper_2006_06762_b200.model import GpuCostModel
-    m = GpuCostModel.from_json(corpus.model_json)
     progs = list(corpus.programs) + _stream_programs()
-    a = m.predict_batch(progs)
-    monkeypatch.setenv("LT_PREDICT_THREAD_PER_ROW", "1")
-    b = m.predict_batch(progs)
-    monkeypatch.delenv("LT_PREDICT_THREAD_PER_ROW")
-    assert np.array_equal(a, b)
-    assert np.array_equal(a[:len(corpus.scores)], corpus.scores)
+    ragged = {"base": 0.25, "n_features": 164, "shrinkage": 0.3, "depth": 3, "trees": [
+        {"eta": 0.3, "feature": [5, -1, 7, -1, -1], "threshold": [0.5, 0, 1.5, 0, 0], "left": [1, 0, 3, 0, 0],
+         "right": [2, 0, 4, 0, 0], "value": [0, 0.125, 0, -2.0, 3.5]},
+        {"eta": 0.3, "feature": [-1], "threshold": [0.0], "left": [0], "right": [0], "value": [0.75]},
+        {"eta": 0.3, "feature": [161, 162, -1, 9, -1, -1, -1], "threshold": [2.0, 1.0, 0, 0.0, 0, 0, 0],
+         "left": [1, 3, 0, 5, 0, 0, 0], "right": [2, 4, 0, 6, 0, 0, 0],
+         "value": [0, 0, 1.0, 0, 2.0, -1.0, 4.0]}]}
+    for mj in (corpus.model_json, ragged):
+        m = GpuCostModel.from_json(mj)
+        X = np.vstack([corpus.features_of(i) for i in range(len(corpus.programs))])
+        X[::7, 5] = np.nan
+        X[::5, 161] = np.nan
+        got = []
+        for env in (None, "LT_PREDICT_IRREGULAR", "LT_PREDICT_THREAD_PER_ROW"):
+            if env:
+                monkeypatch.setenv(env, "1")
+            got.append((m.predict_batch(progs), m.predict_rows(X)))
+            if env:
+                monkeypatch.delenv(env)
+        for a, b in got[1:]:
+            assert np.array_equal(got[0][0], a) and np.array_equal(got[0][1], b, equal_nan=True)
+        from oracle import predict as OP
+        assert np.array_equal(got[0][1], OP.predict_rows(OP.load_model(mj), X), equal_nan=True)
+        if mj is corpus.model_json:
+            assert np.array_equal(got[0][0][:len(corpus.scores)], corpus.scores)
 
 
 def test_c_abi_comm_single_rank_roundtrip():
