@@ -40,6 +40,7 @@ import os
 import pickle
 import sys
 import time
+import weakref
 from collections import OrderedDict
 from dataclasses import dataclass, field, replace
 
@@ -837,6 +838,7 @@ class Runner:
     batch's records (`last_records`) are kept here."""
 
     def __init__(self, device: int = 0, **kw):
+        _LIVE.add(self)
         self.device = device
         self._kw = dict(device=device, **kw)
         self.backend = kw.get("backend", "ptx")
@@ -987,13 +989,16 @@ class Runner:
 
 
 _RUNNER: Runner | None = None
+_LIVE: "weakref.WeakSet[Runner]" = weakref.WeakSet()    # every Runner: each may own a measuring process
 
 
 def _shutdown() -> None:
+    """Close every runner's measuring process (also runners that were replaced
+    by configure() and restarted their process on a later call)."""
     global _RUNNER
-    if _RUNNER is not None:
-        _RUNNER.close()
-        _RUNNER = None
+    for r in list(_LIVE):
+        r.close()
+    _RUNNER = None
 
 
 atexit.register(_shutdown)
