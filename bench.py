@@ -415,6 +415,8 @@ def main() -> None:
     ap.add_argument("--sub-steps", type=int, default=4)
     ap.add_argument("--no-scoring", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines (development runs)")
+    ap.add_argument("--no-stage", action="store_true",
+                    help="do not lower/compile step s+1 behind step s (each step from scratch)")
     ap.add_argument("--compile-workers", type=int, default=0, help="ptxas worker processes per rank (0: auto)")
     ap.add_argument("--lower-workers", type=int, default=0, help="lowering processes per rank (0: auto)")
     args = ap.parse_args()
@@ -459,11 +461,14 @@ def main() -> None:
         sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for ps in progs:
+        for s, ps in enumerate(progs):
             l2_flush.zero_()                   # 256 MB write: no step starts with a warm L2
             if e2e:                            # inputs from pinned host memory, ground truth recomputed
                 runner.refresh()
-            results.append(sharded_measure(ps))          # NCCL all_gather of (status, cost) records
+            # steps are pipelined: the next step's candidates are lowered and compiled
+            # behind this one (never across the edge of the timed region)
+            nxt = progs[s + 1] if (s + 1 < len(progs) and not args.no_stage) else None
+            results.append(sharded_measure(ps, stage=nxt))   # NCCL all_gather of (status, cost) records
             records.append(list(runner.last_records))
         e1.record()
         sync()
@@ -586,6 +591,10 @@ def main() -> None:
                        "stream": f"tests/golden/streams/{args.config}.json.gz (reference sampler, legal launches)",
                        "timed_states": [args.warmup * args.batch * world, need],
                        "compile_workers_per_rank": workers, "cubin_cache": "empty at start", "rate": RATE_DEF,
+                       "pipelined_steps": (not args.no_stage and
+                                           "step s+1's candidates are lowered and compiled behind step s (compile "
+                                           "pool priority: the older step's jobs first); nothing crosses the edges "
+                                           "of the timed region"),
                        "l2": "flushed before every timed step (256 MB write); a candidate's cost is the mean of "
                              "back-to-back repeats after its verified warm-up run"},
             "valid": head["valid"], "measured": head["measured"],

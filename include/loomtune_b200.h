@@ -98,6 +98,8 @@ int lt_pool_start(int n_workers, const char* cache_dir, double timeout_s);
 void lt_pool_stop(void);
 int lt_pool_size(void);
 int64_t lt_compile_submit(const char* src, int64_t len, const char* opts_newline_separated);
+/* queued behind every job with a lower prio (the next batch, compiled ahead of time) */
+int64_t lt_compile_submit_prio(const char* src, int64_t len, const char* opts_newline_separated, int64_t prio);
 int lt_compile_wait(int64_t job, int* status, double* seconds, int* cache_hit, int64_t* out_len);
 int lt_compile_ready(int64_t job);                             /* 1 done, 0 pending, -1 unknown */
 int lt_compile_fetch(int64_t job, char* buf, int64_t cap);   /* cubin, or log when status != 0 */

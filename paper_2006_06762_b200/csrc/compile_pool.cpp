@@ -43,6 +43,7 @@ struct Job {
   int status = 0;
   double secs = 0.0;
   bool cache_hit = false;
+  int64_t prio = 0;  // lower runs first (the batch a job belongs to); then longest first
   std::string result;
   std::chrono::steady_clock::time_point started;
 };
@@ -58,7 +59,7 @@ class Pool {
   ~Pool() { stop(); }
   int start(int n, const std::string& cache_dir, double timeout_s);
   void stop();
-  int64_t submit(const char* src, int64_t len, const char* opts);
+  int64_t submit(const char* src, int64_t len, const char* opts, int64_t prio = 0);
   int wait(int64_t id, int* status, double* secs, int* hit, int64_t* len);
   int fetch(int64_t id, char* buf, int64_t cap);
   int ready(int64_t id) {
@@ -210,8 +211,9 @@ void Pool::stop() {
   cv_done_.notify_all();
 }
 
-int64_t Pool::submit(const char* src, int64_t len, const char* opts) {
+int64_t Pool::submit(const char* src, int64_t len, const char* opts, int64_t prio) {
   Job j;
+  j.prio = prio;
   j.src.assign(src, (size_t)len);
   std::string o = opts ? opts : "";
   size_t p = 0;
@@ -297,10 +299,14 @@ void Pool::loop() {
       for (auto& w : workers_) {
         if (w.job || queue_.empty()) continue;
         if (w.pid < 0 && spawn(w)) continue;
-        // longest job first (source size ~ ptxas time): shortens a batch's tail
+        // the oldest batch first, and within it the longest job first (source
+        // size ~ ptxas time): shortens a batch's tail
         auto best = queue_.begin();
-        for (auto it = queue_.begin(); it != queue_.end(); ++it)
-          if (jobs_[*it].src.size() > jobs_[*best].src.size()) best = it;
+        for (auto it = queue_.begin(); it != queue_.end(); ++it) {
+          const Job& a = jobs_[*it];
+          const Job& b = jobs_[*best];
+          if (a.prio < b.prio || (a.prio == b.prio && a.src.size() > b.src.size())) best = it;
+        }
         int64_t id = *best;
         queue_.erase(best);
         Job& j = jobs_[id];
@@ -405,6 +411,12 @@ int lt_pool_size(void) { return lt::g_pool.size(); }
 
 // opts: newline-separated NVRTC options.  Returns a job id (> 0).
 int64_t lt_compile_submit(const char* src, int64_t len, const char* opts) { return lt::g_pool.submit(src, len, opts); }
+
+// As lt_compile_submit, queued behind every job of a lower priority value (a
+// later batch compiled ahead of time waits for the current batch's jobs).
+int64_t lt_compile_submit_prio(const char* src, int64_t len, const char* opts, int64_t prio) {
+  return lt::g_pool.submit(src, len, opts, prio);
+}
 
 int lt_compile_wait(int64_t job, int* status, double* secs, int* cache_hit, int64_t* out_len) {
   return lt::g_pool.wait(job, status, secs, cache_hit, out_len);

@@ -55,16 +55,21 @@ def _gather_array(local: np.ndarray, n_total: int, rank: int, world: int, dist, 
 
 
 def measure_batch_sharded(programs, spec=None, limits=None, best_cost=None, measure_records=None,
-                          group=None, device=None):
+                          group=None, device=None, stage=None):
     """`measure_batch` over all ranks; `measure_records(programs, seed)` -> Records
-    (defaults to this rank's GPU runner)."""
+    (defaults to this rank's GPU runner).  `stage`: the next batch, whose shard
+    this rank's runner lowers and compiles behind the current one."""
     from .measure import MeasureLimits, Record, get_runner, normalise
     limits = limits if limits is not None else MeasureLimits()
     programs = list(programs)
     rank, world, dist = _world(group)
     seed = getattr(limits, "check_seed", 0)
     if measure_records is None:
-        measure_records = lambda ps, s: get_runner().measure_programs(ps, seed=s)  # noqa: E731
+        nxt = None
+        if stage:
+            s_lo, s_hi = shard_bounds(len(stage), rank, world)
+            nxt = list(stage)[s_lo:s_hi]
+        measure_records = lambda ps, s: get_runner().measure_programs(ps, seed=s, stage=nxt)  # noqa: E731
     lo, hi = shard_bounds(len(programs), rank, world)
     recs = measure_records(programs[lo:hi], seed)
     if world == 1:

@@ -49,7 +49,7 @@ import numpy as np
 from . import runtime as rt
 from .lower import Lowered, LoweringError, lower, reference_lowering
 from .ptxgen import Unsupported, lower_ptx
-from .state import validate
+from .state import history_to_json, validate
 
 VALID, INVALID, TIMEOUT = "valid", "invalid", "timeout"
 GPU_TOL = 1e-4
@@ -345,6 +345,10 @@ class RunnerCore:
                               else int(os.environ.get("LT_LOWER_WORKERS", max(1, min(8, (os.cpu_count() or 2) // 2)))))
         self._lpool = None
         self.faulted = False            # a candidate faulted: this process's CUDA state is lost
+        self._batch_seq = 0             # compile-pool priority of the batch being measured
+        self._stage_thread = None       # lowering + compiling the next batch (see stage)
+        self._staged: dict = {}
+        self._staged_for = -1
         self.force_recompile = False    # test hook: treat every first verification as failed
 
     def _lower_pool(self):
@@ -401,11 +405,11 @@ class RunnerCore:
         return self.ctx[key]
 
     # -- compile + load ------------------------------------------------------
-    def submit(self, source: str, opts: str | None = None) -> int:
+    def submit(self, source: str, opts: str | None = None, prio: int = 0) -> int:
         b = source.encode()
         if opts is None:
             opts = PTX_OPTS if source.startswith(".version") else NVRTC_OPTS
-        return self.lib.lt_compile_submit(b, len(b), opts.encode())
+        return self.lib.lt_compile_submit_prio(b, len(b), opts.encode(), prio)
 
     def lower(self, p) -> Lowered:
         """PTX backend by default; NVRTC (CUDA C) for what PTX does not express."""
@@ -468,14 +472,79 @@ class RunnerCore:
         return out
 
     # -- measurement ---------------------------------------------------------
-    def measure_programs(self, programs: list, seed: int = 0) -> list:
+    def _parts(self, lo: Lowered, batch_keys: dict, prio: int) -> list:
+        """[(entries, kernel key, job | None | ("dup", key))] for one lowered
+        candidate: loaded kernels are reused, a kernel already submitted for this
+        batch is shared, every other kernel module is submitted (priority `prio`)."""
+        parts = []
+        for ents, text, opts in _modules_of(lo):
+            kkey = hashlib.sha1((opts or "").encode() + text.encode()).hexdigest()
+            with self.mod_lock:
+                loaded = kkey in self.modules
+            if loaded:
+                parts.append((ents, kkey, None))
+            elif kkey in batch_keys:                 # same kernel in another candidate
+                parts.append((ents, kkey, ("dup", kkey)))
+                self.stats["kernels_shared"] += 1
+            else:
+                job = self.submit(text, opts, prio)
+                batch_keys[kkey] = job
+                parts.append((ents, kkey, job))
+        return parts
+
+    @staticmethod
+    def _program_key(p, dag_json: dict) -> str:
+        d = dag_json.get(id(p.dag))
+        if d is None:
+            d = dag_json[id(p.dag)] = json.dumps(p.dag.to_json(), sort_keys=True)
+        return hashlib.sha1((d + json.dumps(history_to_json(p.history))).encode()).hexdigest()
+
+    def stage(self, programs: list) -> None:
+        """Start lowering and compiling a LATER batch now, in the background: its
+        compile jobs queue behind every job of the batch being measured (pool
+        priority), so they only fill cores that batch leaves idle (its tail).
+        The next `measure_programs` call picks up whatever is staged for its
+        programs; nothing is measured here."""
+        prio = self._batch_seq + 1
+        staged: dict = {}
+        self._staged_for, self._staged = prio, staged
+
+        def work():
+            dag_json: dict = {}
+            batch_keys: dict = {}
+            for i, p, res in self._lowered(programs):
+                parts = self._parts(res[1], batch_keys, prio) if res[0] == "ok" else None
+                staged[self._program_key(p, dag_json)] = (res, parts)
+        self._stage_thread = threading.Thread(target=work, daemon=True)
+        self._stage_thread.start()
+
+    def measure_programs(self, programs: list, seed: int = 0, stage: list | None = None) -> list:
         """Validate + lower on this thread while a measurement thread drains
-        finished compiles onto the GPU (ctypes drops the GIL inside lt_measure)."""
+        finished compiles onto the GPU (ctypes drops the GIL inside lt_measure).
+        `stage`: the programs of the next batch, lowered and compiled behind this
+        one (see `stage`)."""
         t_start = time.perf_counter()
         self._t_batch = t_start
+        self._batch_seq += 1
+        prio = self._batch_seq
+        staged: dict = {}
+        if self._stage_thread is not None:
+            self._stage_thread.join()
+            self._stage_thread = None
+            if self._staged_for == prio:
+                staged = self._staged
+            self._staged = {}
         recs = [Record() for _ in programs]
         for p in programs:                       # device contexts are created up front
             self.context(p.dag, seed)
+        dag_json: dict = {}
+        ready, fresh = [], []
+        for i, p in enumerate(programs):
+            hit = staged.pop(self._program_key(p, dag_json), None) if staged else None
+            (ready if hit is not None else fresh).append((i, p, hit))
+        self.stats["staged"] = self.stats.get("staged", 0) + len(ready)
+        if stage:
+            self.stage(list(stage))
         q: queue.Queue = queue.Queue()
         worker = threading.Thread(target=self._drain, args=(q, recs, seed), daemon=True)
         worker.start()
@@ -484,10 +553,12 @@ class RunnerCore:
             # compile jobs are submitted as lowerings finish; the pool hands the
             # largest pending source to each free worker (longest-processing-time
             # first), which shortens the batch's tail
-            lowered = self._lowered(programs)
-            if os.environ.get("LT_LOWER_ALL"):
-                lowered = sorted(lowered, key=lambda x: -len(x[2][1].source) if x[2][0] == "ok" else 0)
-            for i, p, (kind_, payload, secs) in lowered:
+            def results():
+                for i, p, (res, parts) in ready:
+                    yield i, p, res, parts
+                for i, p, res in self._lowered([p for _, p, _ in fresh]):
+                    yield fresh[i][0], p, res, None
+            for i, p, (kind_, payload, secs), parts in results():
                 recs[i].lower_s = secs
                 recs[i].t["lowered"] = time.perf_counter() - t_start
                 self.stats["lower_s"] += secs
@@ -499,20 +570,8 @@ class RunnerCore:
                 recs[i].info = lo.info
                 key = hashlib.sha1(lo.source.encode()).hexdigest()
                 recs[i].key = key
-                parts = []
-                for ents, text, opts in _modules_of(lo):
-                    kkey = hashlib.sha1((opts or "") .encode() + text.encode()).hexdigest()
-                    with self.mod_lock:
-                        loaded = kkey in self.modules
-                    if loaded:
-                        parts.append((ents, kkey, None))
-                    elif kkey in batch_keys:                 # same kernel in another candidate
-                        parts.append((ents, kkey, ("dup", kkey)))
-                        self.stats["kernels_shared"] += 1
-                    else:
-                        job = self.submit(text, opts)
-                        batch_keys[kkey] = job
-                        parts.append((ents, kkey, job))
+                if parts is None:
+                    parts = self._parts(lo, batch_keys, prio)
                 q.put((i, p, lo, key, parts))
         finally:
             q.put(None)
@@ -737,12 +796,12 @@ class _Server:
     def __init__(self, kw: dict):
         self.core = RunnerCore(**kw)
 
-    def measure(self, programs, seed):
+    def measure(self, programs, seed, stage=None):
         c = self.core
         if len(c._dag_keys) > 256:         # every call unpickles fresh DAG objects
             c._dag_keys.clear()
         s0, io0 = dict(c.stats), dict(c.io)
-        recs = c.measure_programs(programs, seed)
+        recs = c.measure_programs(programs, seed, stage)
         return recs, _delta(c.stats, s0), _delta(c.io, io0)
 
     def prepare(self, dag, seed):
@@ -916,18 +975,23 @@ class Runner:
             self._reap()
 
     # -- API -------------------------------------------------------------------
-    def measure_programs(self, programs: list, seed: int = 0) -> list:
+    def measure_programs(self, programs: list, seed: int = 0, stage: list | None = None) -> list:
         """Records in input order.  Candidates a fault cut off are measured again
         in a fresh process; if the process dies outright (not a reported fault),
-        the rest is measured one candidate per call so the culprit is isolated."""
+        the rest is measured one candidate per call so the culprit is isolated.
+        `stage`: the next batch's programs, lowered and compiled in the measuring
+        process behind this batch (RunnerCore.stage)."""
         programs = list(programs)
         recs: list = [None] * len(programs)
         todo = list(range(len(programs)))
         solo = False
+        first = True
         while todo:
             chunk = todo[:1] if solo else todo
             try:
-                got, dstats, dio = self._call("measure", [programs[i] for i in chunk], seed)
+                got, dstats, dio = self._call("measure", [programs[i] for i in chunk], seed,
+                                              list(stage) if (stage and first) else None)
+                first = False
             except _ChildDied as e:
                 if len(chunk) == 1:
                     recs[chunk[0]] = Record(detail=f"gpu: {e}", done=True)

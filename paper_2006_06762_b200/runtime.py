@@ -77,6 +77,7 @@ _SIGS = [
     ("lt_pool_stop", None, []),
     ("lt_pool_size", ctypes.c_int, []),
     ("lt_compile_submit", ctypes.c_int64, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_char_p]),
+    ("lt_compile_submit_prio", ctypes.c_int64, [ctypes.c_char_p, ctypes.c_int64, ctypes.c_char_p, ctypes.c_int64]),
     ("lt_compile_wait", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]),
     ("lt_compile_ready", ctypes.c_int, [ctypes.c_int64]),

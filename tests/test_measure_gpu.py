@@ -248,3 +248,23 @@ def test_batch_edge_cases(runner):
     best = min(r.cost for r in res if r.status == VALID)
     assert max(r.throughput for r in res) == 1.0 and all(
         r.throughput == best / r.cost for r in res if r.status == VALID)
+
+
+def test_staged_next_batch(runner):
+    """A batch measured with the next batch staged: the next batch's programs are
+    lowered and compiled behind it, then measured from the staged work with the
+    same verdicts as a from-scratch measurement."""
+    import bench
+    from paper_2006_06762_b200.state import replay
+    dag, stream = bench.load_stream("G10")
+    a = [replay(dag, h) for h in stream[100:116]]
+    b = [replay(dag, h) for h in stream[116:132]]
+    runner.measure_programs(a, stage=b)
+    s0 = runner.stats.get("staged", 0)
+    got = runner.measure_programs(b)
+    assert runner.stats.get("staged", 0) - s0 == len(b)
+    runner.forget_compiled("")
+    want = runner.measure_programs(b)
+    assert [r.status for r in got] == [r.status for r in want]
+    assert [r.key for r in got] == [r.key for r in want]
+    assert all(r.max_rel_err <= 1e-4 for r in got if r.status == "valid")
