@@ -40,7 +40,6 @@ import os
 import pickle
 import sys
 import time
-import weakref
 from collections import OrderedDict
 from dataclasses import dataclass, field, replace
 
@@ -897,7 +896,6 @@ class Runner:
     batch's records (`last_records`) are kept here."""
 
     def __init__(self, device: int = 0, **kw):
-        _LIVE.add(self)
         self.device = device
         self._kw = dict(device=device, **kw)
         self.backend = kw.get("backend", "ptx")
@@ -931,6 +929,7 @@ class Runner:
             proc.join(5)
             raise rt.NativeError(f"measuring process failed to start: {payload}")
         self._proc, self._conn, self.pid = proc, parent, payload
+        _LIVE.add(self)
         if self._max_modules is not None:
             self._call("set_max_modules", self._max_modules)
         for dag, seed in self._prepared:
@@ -945,6 +944,7 @@ class Runner:
                 self._proc.kill()
                 self._proc.join(5)
         self._proc = self._conn = None
+        _LIVE.discard(self)
 
     def _call(self, cmd: str, *args):
         if self._proc is None:
@@ -1053,7 +1053,8 @@ class Runner:
 
 
 _RUNNER: Runner | None = None
-_LIVE: "weakref.WeakSet[Runner]" = weakref.WeakSet()    # every Runner: each may own a measuring process
+_LIVE: set = set()      # Runners that own a live measuring process (strong refs: a dropped Runner's
+                        # process would otherwise outlive it and hang multiprocessing's exit join)
 
 
 def _shutdown() -> None:

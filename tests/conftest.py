@@ -23,4 +23,7 @@ def corpus():
 if os.environ.get("LT_HANG_DUMP"):
     import faulthandler
     import signal
-    faulthandler.register(signal.SIGUSR1, all_threads=True)
+    faulthandler.register(signal.SIGUSR1, all_threads=True, file=sys.__stderr__)
+    # a C watchdog thread: dumps every Python thread and exits if the process is
+    # still alive after LT_HANG_DUMP seconds (also during interpreter teardown)
+    faulthandler.dump_traceback_later(float(os.environ["LT_HANG_DUMP"]), exit=True, file=sys.__stderr__)
