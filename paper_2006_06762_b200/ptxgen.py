@@ -738,10 +738,156 @@ def _dec(g: Ptx, d, lv: dict) -> Aff:
     return Aff.reg(g.udiv(r, d.c) if kk == "DDiv" else g.urem(r, d.c))
 
 
+def _quad_read(mod: _Mod, s):
+    """The elementwise stages the naive template moves four points at a time
+    (16-byte loads and stores): no reduction; the innermost loop is the output's
+    innermost iterator itself (identity decode), its extent a multiple of 4; the
+    body is `Read(buf, idx)` or `Select(cond, Read(buf, idx), 0)` — a copy, or
+    the padding stage — where only idx's innermost dim uses that iterator
+    (coefficient 1, constant a multiple of 4, an unpacked buffer whose innermost
+    extent is a multiple of 4) and cond does not use it.  Returns (iterator,
+    Read, Select or None) or None."""
+    if s.reduce or mod.dtype != "float" or "nquad" in _OFF:
+        return None
+    sp = [l for l in s.loops if l.kind == "space"]
+    if not sp or sp[-1].extent % 4:
+        return None
+    last = sp[-1]
+    space = [n for n, _ in s.space]
+    dmap = dict(s.index_map)
+    n_last = space[-1]
+    d = dmap.get(n_last)
+    if d is None or kind(d) != "DVar" or d.loop != last.id or s.space[-1][1] % 4:
+        return None
+
+    def uses(d2):
+        k2 = kind(d2)
+        if k2 == "DVar":
+            return d2.loop == last.id
+        if k2 == "DConst":
+            return False
+        if k2 == "DAdd":
+            return uses(d2.a) or uses(d2.b)
+        return uses(d2.a)
+    if any(uses(dmap[n]) for n in space[:-1] if n in dmap):
+        return None
+    e = s.expr
+    sel = None
+    if kind(e) == "Select":
+        if kind(e.other) != "Const" or float(e.other.value) != 0.0:
+            return None
+        sel, e = e, e.then
+        if any(n_last in lin_iters(x) for x in _itervals(sel.cond)) or list(reads(sel.cond)):
+            return None
+    if kind(e) != "Read":
+        return None
+    buf = e.buffer
+    if buf in mod.layouts and buf not in mod.live:
+        return None
+    if any(c.name == buf for c in mod.attached(s.name)):       # an inline producer, not in memory
+        return None
+    shape = mod.shape(buf)
+    if shape[-1] % 4:
+        return None
+    for j, lin in enumerate(e.index):
+        c = dict(lin.terms).get(n_last, 0)
+        if j < len(e.index) - 1:
+            if c:
+                return None
+        elif c != 1 or lin.const % 4 or any(n != n_last and cc % 4 for n, cc in lin.terms):
+            return None
+    return n_last, e, sel
+
+
+def _itervals(e):
+    k = kind(e)
+    if k == "IterVal":
+        yield e.lin
+    elif k == "Bin":
+        yield from _itervals(e.lhs)
+        yield from _itervals(e.rhs)
+    elif k in ("Call",):
+        yield from _itervals(e.arg)
+    elif k == "Select":
+        yield from _itervals(e.cond)
+        yield from _itervals(e.then)
+        yield from _itervals(e.other)
+
+
+def lin_iters(lin) -> set:
+    return {n for n, _ in lin.terms}
+
+
+def _naive_quad(mod: _Mod, s, entry: str, plan) -> tuple:
+    """`_naive` for the elementwise stages `_quad_read` accepts: a thread step
+    covers four consecutive innermost points with one 16-byte load (predicated
+    by the padding condition, zero-filled otherwise) and one 16-byte store."""
+    n_last, rd, sel = plan
+    k = _Kern(mod, entry, NAIVE_THREADS)
+    g = k.g
+    sp_loops = [l for l in s.loops if l.kind == "space"]
+    exts = [l.extent for l in sp_loops[:-1]] + [sp_loops[-1].extent // 4]
+    total = 1
+    for x in exts:
+        total *= x
+    if 4 * total + 148 * 16 * NAIVE_THREADS >= (1 << 31):
+        raise Unsupported("index space exceeds 2^31")
+    grid = max(1, min((total + NAIVE_THREADS - 1) // NAIVE_THREADS, 148 * 16))
+    step = grid * NAIVE_THREADS
+    dmap = dict(s.index_map)
+    space_names = [n for n, _ in s.space]
+    tid, cta, pidx = g.new("%r"), g.new("%r"), g.new("%r")
+    g(f"mov.u32 {tid}, %tid.x;")
+    g(f"mov.u32 {cta}, %ctaid.x;")
+    g(f"mad.lo.s32 {pidx}, {cta}, {NAIVE_THREADS}, {tid};")
+    top, done = g.new_label(), g.new_label()
+    pe = g.new("%p")
+    g(f"setp.ge.s32 {pe}, {pidx}, {total};")
+    g(f"@{pe} bra {done};")
+    g.label(top)
+    g.push()
+    digits = g.decompose(pidx, exts)
+    lv = {l.id: Aff.reg(dg) for l, dg in zip(sp_loops, digits)}
+    lv[sp_loops[-1].id] = Aff.reg(digits[-1], 4)
+    env = {n: _dec(g, dmap[n], lv) for n in space_names if n in dmap}
+    ex = Expr(g, lambda n: env[n], None)
+    pred = None
+    if sel is not None:
+        pred = ex.pred(sel.cond)
+        if pred is None:
+            c = ex(sel.cond)
+            pred = g.new("%p")
+            g(f"setp.ne.{g.ft} {pred}, {c}, {g.fconst(0.0)};")
+    base, flat = k.gsource(rd.buffer, [ex.lin(l) for l in rd.index])
+    rb, imm = g.gaddr(base, flat)
+    vals = [g.new(g.fr) for _ in range(4)]
+    if pred is not None:
+        for v in vals:
+            g(f"mov.b32 {v}, 0;")
+    g(f"{'@' + pred + ' ' if pred else ''}ld.global.nc.v4.f32 {{{', '.join(vals)}}}, [{rb}+{imm}];")
+    k.vec_stores = True
+    for u, v in enumerate(vals):
+        k.epilogue(s, {n: (env[n] + u if n == n_last else env[n]) for n in space_names}, v,
+                   mod.must_materialize(s))
+    k.drain_stores(True)
+    k.vec_stores = False
+    g.pop()
+    g(f"add.s32 {pidx}, {pidx}, {step};")
+    g(f"setp.lt.s32 {pe}, {pidx}, {total};")
+    g(f"@{pe} bra {top};")
+    g.label(done)
+    args = _args(k, mod, s)
+    return k, Kernel(entry, grid, NAIVE_THREADS, 0, args, {"template": "naive", "stage": s.name, "points": 4 * total,
+                                                            "points_per_thread_step": 4, "vector": 4})
+
+
 def _naive(mod: _Mod, s, entry: str) -> tuple:
     """One output point per thread-iteration (the State's own loops and decode
     maps, reductions serial), NAIVE_POINTS points per grid-stride step so each
     thread keeps several independent loads / accumulation chains in flight."""
+    plan = _quad_read(mod, s) if NAIVE_POINTS == 1 else None
+    if plan is not None:
+        return _naive_quad(mod, s, entry, plan)
     k = _Kern(mod, entry, NAIVE_THREADS)
     g = k.g
     sp_loops = [l for l in s.loops if l.kind == "space"]
