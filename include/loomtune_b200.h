@@ -102,6 +102,7 @@ int64_t lt_compile_submit(const char* src, int64_t len, const char* opts_newline
 int64_t lt_compile_submit_prio(const char* src, int64_t len, const char* opts_newline_separated, int64_t prio);
 int lt_compile_wait(int64_t job, int* status, double* seconds, int* cache_hit, int64_t* out_len);
 int lt_compile_ready(int64_t job);                             /* 1 done, 0 pending, -1 unknown */
+int lt_compile_wait_any(const int64_t* jobs, int n, double timeout_s);  /* index of a finished job, -1: timeout */
 int lt_compile_fetch(int64_t job, char* buf, int64_t cap);   /* cubin, or log when status != 0 */
 
 /* ---- (A) runner --------------------------------------------------------------

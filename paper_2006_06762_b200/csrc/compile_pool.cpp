@@ -60,6 +60,7 @@ class Pool {
   int start(int n, const std::string& cache_dir, double timeout_s);
   void stop();
   int64_t submit(const char* src, int64_t len, const char* opts, int64_t prio = 0);
+  int wait_any(const int64_t* ids, int n, double timeout_s);
   int wait(int64_t id, int* status, double* secs, int* hit, int64_t* len);
   int fetch(int64_t id, char* buf, int64_t cap);
   int ready(int64_t id) {
@@ -384,6 +385,20 @@ int Pool::wait(int64_t id, int* status, double* secs, int* hit, int64_t* len) {
   return 0;
 }
 
+int Pool::wait_any(const int64_t* ids, int n, double timeout_s) {
+  std::unique_lock<std::mutex> g(mu_);
+  int hit = -1;
+  auto any_done = [&] {
+    for (int i = 0; i < n; ++i) {
+      auto it = jobs_.find(ids[i]);
+      if (it == jobs_.end() || it->second.state == 2) { hit = i; return true; }
+    }
+    return false;
+  };
+  cv_done_.wait_for(g, std::chrono::duration<double>(timeout_s), any_done);
+  return hit;
+}
+
 int Pool::fetch(int64_t id, char* buf, int64_t cap) {
   std::lock_guard<std::mutex> g(mu_);
   auto it = jobs_.find(id);
@@ -411,6 +426,12 @@ int lt_pool_size(void) { return lt::g_pool.size(); }
 
 // opts: newline-separated NVRTC options.  Returns a job id (> 0).
 int64_t lt_compile_submit(const char* src, int64_t len, const char* opts) { return lt::g_pool.submit(src, len, opts); }
+
+// Block until one of the jobs has finished (or is unknown): its index, or -1
+// after timeout_s.  Lets the measuring thread sleep instead of polling.
+int lt_compile_wait_any(const int64_t* jobs, int n, double timeout_s) {
+  return lt::g_pool.wait_any(jobs, n, timeout_s);
+}
 
 // As lt_compile_submit, queued behind every job of a lower priority value (a
 // later batch compiled ahead of time waits for the current batch's jobs).

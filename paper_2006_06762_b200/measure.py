@@ -642,7 +642,12 @@ class RunnerCore:
                     if closed and not waiting:
                         return
                     t0 = time.perf_counter()
-                    time.sleep(0.0005)
+                    jobs = [job for x in waiting for _, _, job in x[4] if isinstance(job, int)]
+                    if jobs:        # sleep in the pool until a compile lands (GIL released)
+                        arr = np.asarray(jobs, np.int64)
+                        self.lib.lt_compile_wait_any(rt.ptr(arr, rt.c_i64p), len(jobs), 0.002)
+                    else:
+                        time.sleep(0.0005)
                     self.stats["idle_s"] += time.perf_counter() - t0
                     continue
                 self._measure_one(waiting.pop(idx), recs, seed)

@@ -81,6 +81,7 @@ _SIGS = [
     ("lt_compile_wait", ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int64)]),
     ("lt_compile_ready", ctypes.c_int, [ctypes.c_int64]),
+    ("lt_compile_wait_any", ctypes.c_int, [c_i64p, ctypes.c_int, ctypes.c_double]),
     ("lt_compile_fetch", ctypes.c_int, [ctypes.c_int64, ctypes.c_char_p, ctypes.c_int64]),
     # runner (csrc/runner.cu)
     ("lt_module_load", ctypes.c_int64, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int64]),
