@@ -642,7 +642,8 @@ class RunnerCore:
                     if closed and not waiting:
                         return
                     t0 = time.perf_counter()
-                    jobs = [job for x in waiting for _, _, job in x[4] if isinstance(job, int)]
+                    jobs = [job for x in waiting for _, _, job in x[4]
+                            if isinstance(job, int) and self.lib.lt_compile_ready(job) == 0]
                     if jobs:        # sleep in the pool until a compile lands (GIL released)
                         arr = np.asarray(jobs, np.int64)
                         self.lib.lt_compile_wait_any(rt.ptr(arr, rt.c_i64p), len(jobs), 0.002)
