@@ -74,12 +74,21 @@ def global_avg_pool(n: int = 16, h: int = 7, c: int = 2048):
     return ComputeDAG((x, s, g))
 
 
-def tasks(batch: int = 16, pools: bool = True):
-    """[(name, dag, weight)] for every distinct subgraph."""
+def tasks(batch: int = 16, pools: bool = True, fusion: str = "conv"):
+    """[(name, dag, weight)] for every distinct subgraph.
+
+    fusion: "conv" — each convolution alone (inference: BN folds into the
+    weights; the residual add and ReLU are elementwise consumers); "conv_bn_relu"
+    — each convolution with its batch-norm affine and ReLU fused as one subgraph
+    (the ConvLayer config's DAG, `state.workloads.conv_bn_relu`), the fusion the
+    paper's Relay partitioning produces for the non-residual convolutions."""
+    if fusion not in ("conv", "conv_bn_relu"):
+        raise ValueError(f"unknown fusion {fusion!r}")
     out = []
     for h, ci, co, k, s, p, cnt in CONVS:
-        name = f"conv{h}_{ci}_{co}_k{k}s{s}"
-        out.append((name, build("conv2d", h=h, w=h, ci=ci, co=co, kernel=k, stride=s, pad=p, n=batch), cnt))
+        name = f"conv{h}_{ci}_{co}_k{k}s{s}" + ("_bn_relu" if fusion == "conv_bn_relu" else "")
+        out.append((name, build(fusion if fusion == "conv_bn_relu" else "conv2d", h=h, w=h, ci=ci, co=co, kernel=k,
+                                stride=s, pad=p, n=batch), cnt))
     out.append(("dense2048_1000", build("matmul", n=batch, m=1000, k=2048), 1))
     if pools:
         out.append(("maxpool112_64_k3s2", max_pool(n=batch), 1))

@@ -54,3 +54,18 @@ def test_resnet50_task_list():
     assert sum(w for _, _, w in tasks) == 56
     for name, dag, _ in tasks:
         assert generate_sketches(dag, structure="SSSRRSRS"), name
+
+
+def test_resnet50_fused_task_list():
+    """The conv+BN+ReLU fusion variant of the task list: same shapes and weights,
+    every task a ConvLayer-style DAG with SSSRRSRS sketches."""
+    from loomtune.sketch import generate_sketches
+    from paper_2006_06762_b200 import resnet50
+    plain = resnet50.tasks()
+    fused = resnet50.tasks(fusion="conv_bn_relu")
+    assert [w for _, _, w in plain] == [w for _, _, w in fused]
+    for (n1, d1, _), (n2, d2, _) in zip(plain, fused):
+        if n1.startswith("conv"):
+            assert n2 == n1 + "_bn_relu" and d2.outputs == ("E",)
+            assert d2.node("C").space == d1.node("C").space
+            assert generate_sketches(d2, structure="SSSRRSRS"), n2

@@ -3,9 +3,9 @@ reference's unchanged multi-task `tune` (gradient task scheduler,
 `src/sched.py:276-375`) over every distinct ResNet-50 subgraph, with the B200
 hot path installed.
 
-  python tools/tune_network.py BUDGET [SEED] [--batch N] [--gpu-sampler] [--gpu-sketches] [--gpu-rules] [--tasks K]
+  python tools/tune_network.py BUDGET [SEED] [--batch N] [--gpu-sampler] [--gpu-sketches] [--gpu-rules] [--tasks K] [--fused]
 
-Tasks come from `paper_2006_06762_b200.resnet50.tasks` (23 conv shapes + the
+Tasks come from `paper_2006_06762_b200.resnet50.tasks` (--fused: each conv with its BN + ReLU; 23 conv shapes + the
 classifier, weights = instance counts).  Under torchrun each rank measures its
 shard of every batch and the records are all-gathered
 (`paper_2006_06762_b200.dist.measure_batch_sharded`); every rank runs the same
@@ -79,7 +79,7 @@ def main() -> None:
             counts["measured"] += 1
             counts["valid"] += rec["status"] == "valid"
 
-    specs = resnet50.tasks(batch)[:n_tasks]
+    specs = resnet50.tasks(batch, fusion="conv_bn_relu" if opt.get("--fused") else "conv")[:n_tasks]
     tasks = []
     t0 = time.perf_counter()
     for name, dag, weight in specs:
