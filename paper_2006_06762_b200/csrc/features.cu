@@ -96,6 +96,87 @@ __device__ bool ast_eval(const int32_t* nodes, int cnt, int one_at, long long& o
   return true;
 }
 
+// Decode-AST evaluation used by both feature kernels: same operations as ast_interval /
+// ast_eval, with the top three stack entries in registers (the decode ASTs of
+// real States need depth <= 4; deeper entries go to a small local array).
+struct RegStack {
+  Iv a, b, c;          // a = top
+  Iv deep[MAX_STACK];
+  int sp;
+  __device__ __forceinline__ void push(Iv v) {
+    if (sp >= 3) deep[sp - 3] = c;
+    c = b; b = a; a = v; ++sp;
+  }
+  __device__ __forceinline__ Iv pop() {
+    Iv v = a;
+    a = b; b = c;
+    if (sp > 3) c = deep[sp - 4];
+    --sp;
+    return v;
+  }
+};
+
+__device__ __forceinline__ bool ast_interval_w(const int32_t* nodes, int cnt, const int32_t* loops, int pos,
+                                               Iv& out) {
+  RegStack st;
+  st.sp = 0;
+  for (int n = 0; n < cnt; ++n) {
+    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
+    if (op == 0) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{0, loop_hi(loops, arg, pos)});
+    } else if (op == 1) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{arg, arg});
+    } else if (op == 2) {
+      if (st.sp < 2) return false;
+      Iv b = st.pop();
+      st.a.lo += b.lo; st.a.hi += b.hi;
+    } else {
+      if (st.sp < 1) return false;
+      Iv a = st.a;
+      const long long c = arg;
+      if (op == 3) st.a = c >= 0 ? Iv{a.lo * c, a.hi * c} : Iv{a.hi * c, a.lo * c};
+      else if (op == 4) st.a = Iv{fdiv(a.lo, c), fdiv(a.hi, c)};
+      else if (op == 5) {
+        if (fdiv(a.lo, c) == fdiv(a.hi, c)) st.a = Iv{fmod_(a.lo, c), fmod_(a.hi, c)};
+        else st.a = Iv{0, c - 1};
+      } else return false;
+    }
+  }
+  if (st.sp != 1) return false;
+  out = st.a;
+  return true;
+}
+
+__device__ __forceinline__ bool ast_eval_w(const int32_t* nodes, int cnt, int one_at, long long& out) {
+  RegStack st;        // lo carries the value
+  st.sp = 0;
+  for (int n = 0; n < cnt; ++n) {
+    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
+    if (op == 0) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{(arg == one_at) ? 1 : 0, 0});
+    } else if (op == 1) {
+      if (st.sp >= MAX_STACK) return false;
+      st.push(Iv{arg, 0});
+    } else if (op == 2) {
+      if (st.sp < 2) return false;
+      Iv b = st.pop();
+      st.a.lo += b.lo;
+    } else {
+      if (st.sp < 1) return false;
+      if (op == 3) st.a.lo *= arg;
+      else if (op == 4) st.a.lo = fdiv(st.a.lo, arg);
+      else if (op == 5) st.a.lo = fmod_(st.a.lo, arg);
+      else return false;
+    }
+  }
+  if (st.sp != 1) return false;
+  out = st.a.lo;
+  return true;
+}
+
 struct View {
   const int32_t* dims;   // -> first dim record
   int n_marks, has_w, rank, n_dims;
@@ -231,7 +312,7 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
   Iv iv[MAX_ITERS];
   bool ok = true;
   for (int it = 0; it < n_iter; ++it)
-    ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, -1, iv[it]);
+    ok &= ast_interval_w(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, -1, iv[it]);
 
   double total = 1.0;
   for (int i = 0; i < n_nest; ++i) total *= (double)nest[4 * i];
@@ -250,9 +331,9 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
   const int inner_own = (n_nest > own_start) ? nest[4 * (n_nest - 1) + 3] : -1;
   long long val0[MAX_ITERS], val1[MAX_ITERS];
   if (inner_own >= 0) {
-    for (int it = 0; it < n_iter; ++it) ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], -1, val0[it]);
+    for (int it = 0; it < n_iter; ++it) ok &= ast_eval_w(nodes + 2 * itab[2 * it], itab[2 * it + 1], -1, val0[it]);
     for (int it = 0; it < n_iter; ++it)
-      ok &= ast_eval(nodes + 2 * itab[2 * it], itab[2 * it + 1], inner_own, val1[it]);
+      ok &= ast_eval_w(nodes + 2 * itab[2 * it], itab[2 * it + 1], inner_own, val1[it]);
   }
   for (int v = 0; v < n_views; ++v) {
     const View& w = views[v];
@@ -329,7 +410,7 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
       for (int it = 0; it < n_iter; ++it) {
         const unsigned long long key = iter_mask[it] & inside;
         if (pos > 0 && key == seen[it]) continue;
-        ok &= ast_interval(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, iv2[it]);
+        ok &= ast_interval_w(nodes + 2 * itab[2 * it], itab[2 * it + 1], loops, pos, iv2[it]);
         seen[it] = key;
         changed = true;
       }
@@ -449,87 +530,6 @@ __device__ __forceinline__ void feature_row(const int32_t* __restrict__ words, c
 constexpr int FW_WARPS = 4;
 constexpr int FW_CHUNK = 16;
 constexpr int FW_LD = NF + 1;            // odd row stride: conflict-free lane-per-column access
-
-// Decode-AST evaluation for the warp kernel: same operations as ast_interval /
-// ast_eval, with the top three stack entries in registers (the decode ASTs of
-// real States need depth <= 4; deeper entries go to a small local array).
-struct RegStack {
-  Iv a, b, c;          // a = top
-  Iv deep[MAX_STACK];
-  int sp;
-  __device__ __forceinline__ void push(Iv v) {
-    if (sp >= 3) deep[sp - 3] = c;
-    c = b; b = a; a = v; ++sp;
-  }
-  __device__ __forceinline__ Iv pop() {
-    Iv v = a;
-    a = b; b = c;
-    if (sp > 3) c = deep[sp - 4];
-    --sp;
-    return v;
-  }
-};
-
-__device__ __forceinline__ bool ast_interval_w(const int32_t* nodes, int cnt, const int32_t* loops, int pos,
-                                               Iv& out) {
-  RegStack st;
-  st.sp = 0;
-  for (int n = 0; n < cnt; ++n) {
-    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
-    if (op == 0) {
-      if (st.sp >= MAX_STACK) return false;
-      st.push(Iv{0, loop_hi(loops, arg, pos)});
-    } else if (op == 1) {
-      if (st.sp >= MAX_STACK) return false;
-      st.push(Iv{arg, arg});
-    } else if (op == 2) {
-      if (st.sp < 2) return false;
-      Iv b = st.pop();
-      st.a.lo += b.lo; st.a.hi += b.hi;
-    } else {
-      if (st.sp < 1) return false;
-      Iv a = st.a;
-      const long long c = arg;
-      if (op == 3) st.a = c >= 0 ? Iv{a.lo * c, a.hi * c} : Iv{a.hi * c, a.lo * c};
-      else if (op == 4) st.a = Iv{fdiv(a.lo, c), fdiv(a.hi, c)};
-      else if (op == 5) {
-        if (fdiv(a.lo, c) == fdiv(a.hi, c)) st.a = Iv{fmod_(a.lo, c), fmod_(a.hi, c)};
-        else st.a = Iv{0, c - 1};
-      } else return false;
-    }
-  }
-  if (st.sp != 1) return false;
-  out = st.a;
-  return true;
-}
-
-__device__ __forceinline__ bool ast_eval_w(const int32_t* nodes, int cnt, int one_at, long long& out) {
-  RegStack st;        // lo carries the value
-  st.sp = 0;
-  for (int n = 0; n < cnt; ++n) {
-    const int op = nodes[2 * n], arg = nodes[2 * n + 1];
-    if (op == 0) {
-      if (st.sp >= MAX_STACK) return false;
-      st.push(Iv{(arg == one_at) ? 1 : 0, 0});
-    } else if (op == 1) {
-      if (st.sp >= MAX_STACK) return false;
-      st.push(Iv{arg, 0});
-    } else if (op == 2) {
-      if (st.sp < 2) return false;
-      Iv b = st.pop();
-      st.a.lo += b.lo;
-    } else {
-      if (st.sp < 1) return false;
-      if (op == 3) st.a.lo *= arg;
-      else if (op == 4) st.a.lo = fdiv(st.a.lo, arg);
-      else if (op == 5) st.a.lo = fmod_(st.a.lo, arg);
-      else return false;
-    }
-  }
-  if (st.sp != 1) return false;
-  out = st.a.lo;
-  return true;
-}
 
 constexpr int FW_REC = 768;        // statement record words staged in shared memory (longest seen: 635)
 constexpr int FW_TAB = 192;        // memoised (position, iterator) intervals (largest seen: 14 x 8)
