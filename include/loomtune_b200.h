@@ -145,6 +145,11 @@ int lt_host_register(void* host, int64_t bytes);
 int lt_host_unregister(void* host);
 /* fill n 32-bit words of a slot with `value`, stream-ordered (NaN-poisoning scratch) */
 int lt_task_fill(int64_t task, int slot, int64_t n, uint32_t value);
+/* physical copy of a packed constant on the device (replaces the host-side packing of
+   LayoutRewrite constants, src/ir.py:747-760): dst[i] = src[sum_j digit_j(i) * src_mult[j]],
+   digits of i over phys_ext (outer to inner, n_phys <= 16) */
+int lt_task_pack(int64_t task, int dst_slot, int src_slot, int n_phys, const int64_t* phys_ext,
+                 const int64_t* src_mult);
 int lt_task_run(int64_t task, const lt_launch* launches, int n);
 int lt_measure(int64_t task, const lt_launch* launches, int n_launch, const int32_t* check_pairs,
                const int64_t* numel, int n_check, int min_repeat, int max_repeat, double min_ms,

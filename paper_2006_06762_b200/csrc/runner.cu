@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #include <math.h>
 #include <string>
@@ -134,6 +135,30 @@ __global__ void fill_u32_kernel(unsigned int* p, int64_t n, unsigned int v) {
     p[i] = v;
 }
 
+// Physical copy of a packed constant (LayoutRewrite, src/ir.py:747-760): physical
+// element i, decomposed over the descriptor's extents (innermost last), reads the
+// logical element sum_j digit_j * mult_j.  Pure data movement: equal bit for bit to
+// the host restatement measure.pack.  Consecutive threads write consecutive
+// physical words (coalesced stores; the gather is the layout change itself).
+constexpr int PACK_MAX_DIMS = 16;
+struct PackDesc {
+  int n;
+  int64_t ext[PACK_MAX_DIMS];
+  int64_t mult[PACK_MAX_DIMS];
+};
+
+__global__ void pack_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n, PackDesc d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i, off = 0;
+    for (int j = d.n - 1; j >= 0; --j) {
+      int64_t q = r / d.ext[j];
+      off += (r - q * d.ext[j]) * d.mult[j];
+      r = q;
+    }
+    dst[i] = src[off];
+  }
+}
+
 }  // namespace lt
 
 using lt::Task;
@@ -215,6 +240,20 @@ int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads
 
 int64_t lt_task_create(int device) {
   if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return 0;
+  // Keep the local-memory reservation at its high-water mark: by default the driver
+  // shrinks it again after a launch that grew it, so every spilling candidate paid
+  // a device-synchronising reallocation per launch (LT_LMEM_SHRINK=1 restores that).
+  static bool lmem_set[64] = {};
+  if (device >= 0 && device < 64 && !lmem_set[device]) {
+    lmem_set[device] = true;
+    const char* e = getenv("LT_LMEM_SHRINK");
+    if (!(e && e[0] == '1')) {
+      unsigned int fl = 0;
+      cudaGetDeviceFlags(&fl);
+      cudaSetDeviceFlags((fl & ~cudaDeviceMapHost) | cudaDeviceLmemResizeToMax);
+      cudaGetLastError();
+    }
+  }
   Task* t = new Task();
   t->device = device;
   if (lt::check_cuda(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream") ||
@@ -313,6 +352,33 @@ int lt_task_fill(int64_t handle, int slot, int64_t n, uint32_t value) {
   if (it == t->slots.end() || it->second.second < n * 4) return lt::fail("fill: bad slot");
   lt::fill_u32_kernel<<<256, 256, 0, t->stream>>>((unsigned int*)it->second.first, n, value);
   return lt::check_launch("fill");
+}
+
+// Pack slot `src_slot` (fp32, logical row-major) into `dst_slot` through the
+// physical descriptor: n_phys extents (outer to inner) and per-extent multipliers
+// into the logical flat offset.  Stream-ordered on the task stream.
+int lt_task_pack(int64_t handle, int dst_slot, int src_slot, int n_phys, const int64_t* phys_ext,
+                 const int64_t* src_mult) {
+  Task* t = (Task*)(intptr_t)handle;
+  TASK_SCOPE(t);
+  if (n_phys < 1 || n_phys > lt::PACK_MAX_DIMS) return lt::fail("pack: 1..16 physical dims");
+  auto dst = t->slots.find(dst_slot), src = t->slots.find(src_slot);
+  if (dst == t->slots.end() || src == t->slots.end()) return lt::fail("pack: bad slot");
+  lt::PackDesc d;
+  d.n = n_phys;
+  int64_t n = 1, hi = 0;
+  for (int j = 0; j < n_phys; ++j) {
+    if (phys_ext[j] < 1 || src_mult[j] < 0) return lt::fail("pack: bad descriptor");
+    d.ext[j] = phys_ext[j];
+    d.mult[j] = src_mult[j];
+    n *= phys_ext[j];
+    hi += (phys_ext[j] - 1) * src_mult[j];
+  }
+  if (dst->second.second < n * 4 || src->second.second < (hi + 1) * 4) return lt::fail("pack: slot too small");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  lt::pack_kernel<<<(int)blocks, 256, 0, t->stream>>>((float*)dst->second.first, (const float*)src->second.first, n, d);
+  return lt::check_launch("pack");
 }
 
 static int launch_list(Task* t, const lt_launch* ls, int n, std::string& why) {

@@ -107,6 +107,32 @@ def random_inputs(dag, seed: int) -> dict:
     return {n.name: rng.uniform(0.25, 1.0, size=n.shape) for n in dag.nodes if n.is_placeholder}
 
 
+def pack_strides(shape, desc) -> tuple:
+    """Device packing parameters of a packed constant (`lt_task_pack`): the physical
+    extents (outer to inner) and, per physical dim, the step it makes in the flat
+    row-major offset of the logical array -- the same index map as `pack`."""
+    shape = tuple(int(x) for x in shape)
+    lst = [1] * len(shape)
+    for d in range(len(shape) - 2, -1, -1):
+        lst[d] = lst[d + 1] * shape[d + 1]
+    ext, mult = [], []
+    for j, (d, e) in enumerate(desc):
+        st = 1
+        for d2, e2 in desc[j + 1:]:
+            if d2 == d:
+                st *= e2
+        ext.append(int(e))
+        mult.append(st * lst[d])
+    for d in range(len(shape)):
+        tot = 1
+        for d2, e2 in desc:
+            if d2 == d:
+                tot *= e2
+        if tot != shape[d]:
+            raise ValueError(f"packed layout {desc} does not tile dim {d} of {shape}")
+    return np.asarray(ext, np.int64), np.asarray(mult, np.int64)
+
+
 def pack(arr: np.ndarray, desc) -> np.ndarray:
     """Physical layout of a packed constant (LayoutRewrite, `src/ir.py:747-760`):
     one physical dim per descriptor entry, outer to inner."""
@@ -140,7 +166,7 @@ class _DagContext:
         self.slots: dict = {}
         self.sizes: dict = {}
         self.pinned: list = []
-        self.packed: dict = {}          # slot key -> packed host copy (Ansor packs constants once)
+        self.packed: dict = {}          # slot key -> (source, descriptor) its device copy currently holds
         self.inputs = random_inputs(dag, seed)
         self.h2d_bytes = 0
         # host copies of the inputs, page-locked once: every upload (the first and
@@ -173,8 +199,7 @@ class _DagContext:
         of an end-to-end run."""
         for key, h in self.host.items():
             self._upload(key, h)
-        for key, host in self.packed.items():           # same slots; packed once on the host
-            self._upload(key, host)
+        self.packed.clear()                             # re-packed on the device at next use
         ref, funcs = self._ref
         launches = self._launches(ref, funcs, fp64=True)
         rt.check(self.r.lib.lt_task_run(self.task, ctypes.addressof(launches), len(ref.kernels)), "ground truth")
@@ -210,13 +235,18 @@ class _DagContext:
         if b.role == "input":
             return self.slots[f"in64:{b.name}" if fp64 else f"in:{b.name}"]
         if b.role == "packed":
-            key = f"pk:{b.source}:{b.desc}"
-            if key not in self.slots:
-                host = np.ascontiguousarray(pack(self.inputs[b.source], b.desc), dtype=np.float32)
-                self._pin(host)
-                self._upload(key, host)
-                self.packed[key] = host
-            return self.slots[key]
+            # one slot per packed buffer name, re-laid out on the device (a stream-ordered
+            # gather, microseconds) whenever a candidate asks for another descriptor: no
+            # host packing, no pinning, no allocation per layout
+            key = f"pk:{b.name}"
+            sid = self.slot(key, b.numel * 4)
+            if self.packed.get(key) != (b.source, b.desc):
+                ext, mult = pack_strides(self.inputs[b.source].shape, b.desc)
+                rt.check(self.r.lib.lt_task_pack(self.task, sid, self.slots[f"in:{b.source}"], len(ext),
+                                                 rt.ptr(ext, rt.c_i64p), rt.ptr(mult, rt.c_i64p)),
+                         "pack constant")
+                self.packed[key] = (b.source, b.desc)
+            return sid
         if fp64:
             return self.slots[f"ref:{b.name}"]
         return self.slot(f"buf:{b.name}", b.numel * 4)
@@ -236,6 +266,7 @@ class _DagContext:
 
     def measure(self, lo: Lowered, funcs: list, min_ms: float, max_repeat: int,
                 min_repeat: int = 1) -> rt.MeasureRecord:
+        t0 = time.perf_counter()
         launches = self._launches(lo, funcs)
         pairs, numel = [], []
         for name in lo.outputs:
@@ -251,9 +282,13 @@ class _DagContext:
         pairs_a = np.asarray(pairs, np.int32)
         numel_a = np.asarray(numel, np.int64)
         rec = rt.MeasureRecord()
+        t1 = time.perf_counter()
         rt.check(self.r.lib.lt_measure(self.task, ctypes.addressof(launches), len(lo.kernels),
                                        rt.ptr(pairs_a, rt.c_i32p), rt.ptr(numel_a, rt.c_i64p), len(numel),
                                        min_repeat, max_repeat, min_ms, ctypes.addressof(rec)), "lt_measure")
+        st = self.r.stats
+        st["prep_s"] += t1 - t0
+        st["lt_measure_s"] += time.perf_counter() - t1
         return rec
 
     def download(self, name: str, numel: int, fp64: bool = False) -> np.ndarray:
@@ -336,7 +371,8 @@ class RunnerCore:
         self._drain_error = None
         self.stats = {"compiled": 0, "recompiled": 0, "cache_hits": 0, "compile_s": 0.0, "measured": 0,
                       "kernels_compiled": 0, "kernels_shared": 0,
-                      "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0}
+                      "lower_s": 0.0, "gpu_s": 0.0, "load_s": 0.0, "idle_s": 0.0, "wall_s": 0.0,
+                      "prep_s": 0.0, "lt_measure_s": 0.0}
         self.io = {"h2d": 0, "d2h": 0}      # host<->device bytes (inputs, cubins, launch lists / errors)
         self.last_records: list = []
         self.max_modules = 512          # loaded candidate modules kept (LRU)

@@ -56,6 +56,7 @@ _SIGS = [
     ("lt_init", ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
     ("lt_shutdown", ctypes.c_int, []),
     ("lt_task_fill", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_uint32]),
+    ("lt_task_pack", ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_i64p, c_i64p]),
     ("lt_host_register", ctypes.c_int, [ctypes.c_void_p, ctypes.c_int64]),
     ("lt_host_unregister", ctypes.c_int, [ctypes.c_void_p]),
     # multi-GPU exchange for C callers (csrc/comm.cu)

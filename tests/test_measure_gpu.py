@@ -268,3 +268,36 @@ def test_staged_next_batch(runner):
     assert [r.status for r in got] == [r.status for r in want]
     assert [r.key for r in got] == [r.key for r in want]
     assert all(r.max_rel_err <= 1e-4 for r in got if r.status == "valid")
+
+
+def test_device_packing_equals_host_pack():
+    """Packed constants (LayoutRewrite) are laid out on the device by `lt_task_pack`
+    from the resident fp32 input; every physical copy equals the host restatement
+    `measure.pack` bit for bit, and the candidates that read them verify."""
+    import ctypes
+    from bench import load_stream
+    from paper_2006_06762_b200 import measure
+    from paper_2006_06762_b200.state import replay
+    seen = 0
+    for cfg in ("G10", "RC"):
+        dag, stream = load_stream(cfg)
+        core = measure.RunnerCore(device=0, cache_dir="")
+        try:
+            recs = core.measure_programs([replay(dag, h) for h in stream[:24]])
+            assert all(r.status == "valid" for r in recs), [r.detail for r in recs if r.status != "valid"]
+            ctx = core.context(dag, 0)
+            for h in stream[24:40]:
+                lo = core.lower(replay(dag, h))
+                for b in lo.buffers.values():
+                    if b.role != "packed":
+                        continue
+                    sid = ctx.buffer_slot(b, False)
+                    want = np.ascontiguousarray(measure.pack(ctx.inputs[b.source], b.desc), dtype=np.float32).ravel()
+                    got = np.empty_like(want)
+                    assert core.lib.lt_task_download(ctx.task, sid, got.ctypes.data_as(ctypes.c_void_p),
+                                                     got.nbytes) == 0
+                    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), b.desc
+                    seen += 1
+        finally:
+            core.close()
+    assert seen >= 10

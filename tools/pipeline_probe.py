@@ -53,6 +53,7 @@ def main() -> None:
            "valid": len(valid), "wall_s": st["wall_s"], "rate": args.k / st["wall_s"],
            "compile_s_sum": sum(x.compile_s for x in recs), "lower_s_sum": sum(x.lower_s for x in recs),
            "gpu_s": st["gpu_s"], "idle_s": st["idle_s"], "kernel_s_sum": sum(dev_us) / 1e6,
+           "prep_s": st.get("prep_s"), "lt_measure_s": st.get("lt_measure_s"),
            "first_us_p50": pct([x.first_us for x in valid], 0.5), "first_us_p90": pct([x.first_us for x in valid], 0.9),
            "first_us_max": max((x.first_us for x in valid), default=None),
            "compile_s_p50": pct([x.compile_s for x in recs], 0.5), "compile_s_p90": pct([x.compile_s for x in recs], 0.9),
