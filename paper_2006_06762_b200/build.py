@@ -2,7 +2,8 @@
 
 `python -m paper_2006_06762_b200.build` (or `__graft_entry__.build()`) writes
 `paper_2006_06762_b200/_lib/libloomtune_b200.so` plus the NVRTC compile worker
-`paper_2006_06762_b200/_lib/lt_nvrtc_worker`.  Objects are rebuilt only when a
+`paper_2006_06762_b200/_lib/lt_nvrtc_worker` and the native State encoder
+`paper_2006_06762_b200/_lib/_lt_encode*.so` (CPython extension, g++).  Objects are rebuilt only when a
 source is newer than its output.
 """
 
@@ -11,6 +12,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -18,6 +20,7 @@ LIBDIR = os.path.join(HERE, "_lib")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(LIBDIR, "libloomtune_b200.so")
 WORKER = os.path.join(LIBDIR, "lt_nvrtc_worker")
+ENCODER = os.path.join(LIBDIR, "_lt_encode" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -74,6 +77,10 @@ def build(verbose: bool = False) -> str:
         _run(["g++", "-O2", "-std=c++17", "-I", os.path.join(CUDA, "include"), wsrc, "-o", WORKER,
               "-L", os.path.join(CUDA, "lib64"), "-lnvrtc", "-lnvptxcompiler_static", "-lpthread", "-lm",
               "-Wl,-rpath," + os.path.join(CUDA, "lib64")])
+    esrc = os.path.join(CSRC, "encode_ext.cpp")
+    if os.path.exists(esrc) and _stale(ENCODER, [esrc, __file__]):
+        _run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-fvisibility=hidden",
+              "-I", sysconfig.get_paths()["include"], esrc, "-o", ENCODER])
     return LIB
 
 

@@ -207,8 +207,39 @@ def encode_program(p, out: list, ops_cache: dict, gpu_features: bool = False) ->
     return len(live)
 
 
-def encode_batch(programs, gpu_features: bool = False) -> tuple:
-    """-> (words int32[], stmt_offsets int64[n_stmt+1], prog_row_offsets int64[n_prog+1])."""
+def _native():
+    """The native encoder (`csrc/encode_ext.cpp`, built in-tree by build.py): the same
+    records as `encode_program`, produced by C++ walking the reference's objects."""
+    global _NATIVE
+    if _NATIVE is None:
+        import importlib.util
+        import glob
+        import os
+        lib = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+        hits = glob.glob(os.path.join(lib, "_lt_encode*.so"))
+        if not hits:
+            raise ImportError(f"native encoder not built in {lib} (run python -m paper_2006_06762_b200.build)")
+        spec = importlib.util.spec_from_file_location("_lt_encode", hits[0])
+        mod = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(mod)
+        mod.set_error(EncodeError)
+        _NATIVE = mod
+    return _NATIVE
+
+
+_NATIVE = None
+
+
+def encode_batch(programs, gpu_features: bool = False, native: bool | None = None) -> tuple:
+    """-> (words int32[], stmt_offsets int64[n_stmt+1], prog_row_offsets int64[n_prog+1]).
+    The native encoder runs unless gpu_features is asked (its kernel-binding words come
+    from the lowering, in Python) or native=False / LT_PY_ENCODER=1 (A/B and tests)."""
+    if native is None:
+        import os
+        native = os.environ.get("LT_PY_ENCODER", "") != "1"
+    if native and not gpu_features:
+        w, so, po = _native().encode_batch(list(programs))
+        return np.frombuffer(w, np.int32), np.frombuffer(so, np.int64), np.frombuffer(po, np.int64)
     recs: list = []
     prog_off = [0]
     cache: dict = {}

@@ -40,6 +40,36 @@ def test_encoder_records(corpus):
         assert 0 <= r[1] <= r[0] <= 32 and r[2] <= 64 and r[3] <= 24 and 1 <= r[4] <= 12
 
 
+def test_native_encoder_equals_python_encoder(corpus):
+    """The native encoder (csrc/encode_ext.cpp, the default) writes exactly the
+    records of encode.py's Python restatement: the golden corpus (incl. evolved,
+    rfactor, cache and packed States), stream slices of every config, and the
+    error raised for a decode over an unknown loop."""
+    from paper_2006_06762_b200 import build as B
+    B.build()
+    import bench
+    from paper_2006_06762_b200.state import replay
+    sets = [list(corpus.programs)]
+    for cfg in ("RC", "G10", "CL", "TBG"):
+        dag, stream = bench.load_stream(cfg)
+        sets.append([replay(dag, h) for h in stream[:200]])
+    for progs in sets:
+        a = encode.encode_batch(progs, native=False)
+        b = encode.encode_batch(progs, native=True)
+        for x, y in zip(a, b):
+            assert x.dtype == y.dtype and np.array_equal(x, y)
+    import dataclasses
+
+    import loomtune.ir as IR
+    p = corpus.programs[0]
+    s0 = next(s for s in p.stages if s.index_map)
+    bad = dataclasses.replace(s0, index_map=((s0.index_map[0][0], IR.DVar("nope")),) + tuple(s0.index_map[1:]))
+    q = dataclasses.replace(p, stages=tuple(bad if s is s0 else s for s in p.stages))
+    for native in (False, True):
+        with pytest.raises(encode.EncodeError, match="unknown loop 'nope'"):
+            encode.encode_batch([q], native=native)
+
+
 def test_lowering_covers_corpus(corpus):
     ok = illegal = 0
     for p in corpus.programs:
