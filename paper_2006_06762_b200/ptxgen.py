@@ -187,7 +187,19 @@ class Ptx:
         r = None
         # oldest registers first: the loop-invariant prefix of the chain is then
         # hoistable by ptxas out of rolled loops
-        for reg, c in sorted(a.terms.items(), key=_reg_order if "order" not in _OFF else None):
+        terms = sorted(a.terms.items(), key=_reg_order if "order" not in _OFF else None)
+        start = 0
+        if "prefix" not in _OFF:
+            # every partial sum of two or more terms is value-numbered: chains that share
+            # a prefix (each fetch trip's address = the same block / stage part + its own
+            # digits) reuse it instead of re-emitting it (smaller PTX, less ptxas time)
+            for j in range(len(terms), 1, -1):
+                hit = self.cached(("affp", tuple(terms[:j])))
+                if hit:
+                    r, start = hit, j
+                    break
+        for j in range(start, len(terms)):
+            reg, c = terms[j]
             if r is None:
                 if c == 1:
                     r = reg
@@ -196,8 +208,13 @@ class Ptx:
                     self(f"mul.lo.s32 {r}, {reg}, {c};")
             else:
                 nr = self.new("%r")
-                self(f"mad.lo.s32 {nr}, {reg}, {c}, {r};")
+                if c == 1:
+                    self(f"add.s32 {nr}, {reg}, {r};")
+                else:
+                    self(f"mad.lo.s32 {nr}, {reg}, {c}, {r};")
                 r = nr
+                if "prefix" not in _OFF:
+                    self.remember(("affp", tuple(terms[:j + 1])), r)
         if r is None:
             r = self.new("%r")
             self(f"mov.s32 {r}, {a.const};")
