@@ -2,7 +2,7 @@
 into profiles/r02_tuned_best.json: per config the best program over all seeds,
 plus every seed's best in `seeds` (the seed spread).
 
-  python tools/merge_tuned_best.py [GLOB]
+  python tools/merge_tuned_best.py [GLOB] [--fresh]
 """
 
 import glob
@@ -15,10 +15,13 @@ ROOT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
 
 
 def main():
-    pattern = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "tune_*.json.gz")
-    out = {}
-    for path in sorted(glob.glob(pattern)):
-        with gzip.open(path, "rt") as fh:
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    pattern = args[0] if args else os.path.join(ROOT, "gpurun_out", "tune_*.json.gz")
+    path = os.path.join(ROOT, "profiles", "r02_tuned_best.json")
+    # seeds already merged (earlier tune batches whose outputs are gone) are kept
+    out = json.load(open(path)) if "--fresh" not in sys.argv and os.path.exists(path) else {}
+    for tpath in sorted(glob.glob(pattern)):
+        with gzip.open(tpath, "rt") as fh:
             d = json.load(fh)
         cfg = d["config"]
         entry = {"best_us": d["best_us"], "best_tflops": d["best_tflops"], "seed": d["seed"],
@@ -27,13 +30,12 @@ def main():
                            f"{' --gpu-rules' if d.get('gpu_rules') else ' --gpu-sketches'} (round 2)",
                  "history": d["best_history"]}
         cur = out.get(cfg)
-        seeds = (cur or {}).get("seeds", []) + [{k: entry[k] for k in ("seed", "best_us", "best_tflops", "trials",
-                                                                          "wall_s", "source")}]
+        seeds = [x for x in (cur or {}).get("seeds", []) if x["seed"] != entry["seed"]]
+        seeds += [{k: entry[k] for k in ("seed", "best_us", "best_tflops", "trials", "wall_s", "source")}]
         if cur is None or entry["best_us"] < cur["best_us"]:
             cur = entry
         cur["seeds"] = sorted(seeds, key=lambda x: x["seed"])
         out[cfg] = cur
-    path = os.path.join(ROOT, "profiles", "r02_tuned_best.json")
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)
     for c, v in out.items():
