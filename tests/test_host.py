@@ -161,6 +161,44 @@ def test_pack_matches_reference_semantics():
                     assert P[a, b, c, d] == B[b * 4 + d, a * 4 + c]
 
 
+def test_device_pack_parameters_reproduce_pack():
+    """`lt_task_pack`'s index map (physical digits x `pack_strides` multipliers into the
+    flat logical offset), emulated in numpy, equals the host restatement `pack` on
+    every packed layout of the golden streams; a descriptor that does not tile its
+    dims is refused."""
+    import bench
+    from paper_2006_06762_b200.measure import pack, pack_strides, random_inputs
+    from paper_2006_06762_b200.ptxgen import lower_ptx
+    from paper_2006_06762_b200.state import replay
+    seen = set()
+    for cfg in ("G10", "RC", "TBG", "CL"):
+        dag, stream = bench.load_stream(cfg)
+        inputs = random_inputs(dag, 0)
+        for h in stream[:48]:
+            p = replay(dag, h)
+            if validate(p):
+                continue
+            try:
+                lo = lower_ptx(p)
+            except Exception:
+                continue
+            for b in lo.buffers.values():
+                if b.role != "packed" or (b.source, b.desc) in seen:
+                    continue
+                seen.add((b.source, b.desc))
+                a = inputs[b.source].astype(np.float32)
+                ext, mult = pack_strides(a.shape, b.desc)
+                r = np.arange(int(np.prod(ext)))
+                off = np.zeros_like(r)
+                for j in range(len(ext) - 1, -1, -1):
+                    off += (r % ext[j]) * mult[j]
+                    r //= ext[j]
+                assert np.array_equal(a.reshape(-1)[off], np.ascontiguousarray(pack(a, b.desc)).reshape(-1))
+    assert len(seen) >= 20
+    with pytest.raises(ValueError, match="does not tile"):
+        pack_strides((8, 12), ((1, 3), (0, 2), (1, 4), (0, 3)))
+
+
 def test_ptx_backend_legality_and_assembly(corpus, tmp_path):
     """PTX and CUDA-C lowerings agree on legality; generated PTX assembles (ptxas, no GPU)."""
     import subprocess

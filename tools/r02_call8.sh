@@ -13,3 +13,6 @@ done
 timeout 600 ncu --set full --clock-control none --nvtx --nvtx-include "profile/" -c 3 -o gpurun_out/c8_scoring -f \
     python tools/profile_scoring.py 1 > /dev/null 2>&1
 python tools/profile_scoring.py > gpurun_out/c8_scoring_time.log 2>&1
+# shared-load lookahead A/B on the best-found programs (default 64)
+for la in 16 32 128; do LT_LOOKAHEAD=$la timeout 300 python tools/best_found.py RC,G10,CL,TBG > gpurun_out/c8_la$la.log 2>&1; done
+timeout 300 python tools/best_found.py RC,G10,CL,TBG > gpurun_out/c8_la64.log 2>&1
