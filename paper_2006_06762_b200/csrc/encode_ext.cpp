@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <string_view>
 #include <unordered_map>
 #include <utility>
 #include <vector>
@@ -87,12 +88,36 @@ int64_t as_i64(PyObject* o) {
   return v;
 }
 
-std::string as_str(PyObject* o) {
+// UTF-8 view of a str attribute; the objects it points into are owned by the
+// programs being encoded, which the caller keeps alive for the whole call
+using Str = std::string_view;
+
+Str as_str(PyObject* o) {
   Py_ssize_t n;
   const char* s = PyUnicode_AsUTF8AndSize(o, &n);
   if (!s) throw PyErrSet{};
-  return std::string(s, (size_t)n);
+  return Str(s, (size_t)n);
 }
+
+// small insertion-ordered map with dict assignment semantics (d[k] = v overwrites)
+template <class V>
+struct FlatMap {
+  std::vector<std::pair<Str, V>> v;
+  V* find(Str k) {
+    for (auto& e : v)
+      if (e.first == k) return &e.second;
+    return nullptr;
+  }
+  const V* find(Str k) const {
+    for (auto& e : v)
+      if (e.first == k) return &e.second;
+    return nullptr;
+  }
+  void set(Str k, V val) {
+    if (V* x = find(k)) *x = std::move(val);
+    else v.emplace_back(k, std::move(val));
+  }
+};
 
 bool truthy(PyObject* o) {
   int t = PyObject_IsTrue(o);
@@ -133,7 +158,7 @@ struct Seq {
 };
 
 struct LoopInfo {
-  std::string id;
+  Str id;
   int64_t extent;      // int(extent or 1)
   int kind;            // 0 space, 1 reduce
   int ann;             // 0 None/other, 1 parallel, 2 vectorize
@@ -141,10 +166,10 @@ struct LoopInfo {
 
 struct StageInfo {
   PyObject* obj;       // borrowed (the program's stage tuple holds it)
-  std::string name;
+  Str name;
   bool inlined;
   bool has_at;
-  std::string at_stage, at_loop;
+  Str at_stage, at_loop;
   bool loaded = false;          // loops / shape read (live stages, attach targets, read buffers)
   std::vector<LoopInfo> loops;
   std::vector<int64_t> shape;   // tuple(e for _, e in space)
@@ -174,25 +199,25 @@ LoopInfo read_loop(PyObject* l) {
   Ref an = attr(l, N.annotation);
   L.ann = 0;
   if (an.get() != Py_None) {
-    std::string s = as_str(an.get());
+    Str s = as_str(an.get());
     L.ann = s == "parallel" ? 1 : s == "vectorize" ? 2 : 0;
   }
   return L;
 }
 
 // postfix form of a decode AST (encode._postfix): operands before operators
-void postfix(PyObject* d, const std::unordered_map<std::string, int>& loop_idx, std::vector<int32_t>& out) {
+void postfix(PyObject* d, const FlatMap<int>& loop_idx, std::vector<int32_t>& out) {
   int k = kind_of(d);
   switch (k) {
     case K_DVAR: {
-      std::string lp = as_str(attr(d, N.loop).get());
-      auto it = loop_idx.find(lp);
-      if (it == loop_idx.end()) {
+      Ref lpo = attr(d, N.loop);
+      const int* it = loop_idx.find(as_str(lpo.get()));
+      if (!it) {
         std::string r = PyUnicode_AsUTF8(Ref(PyObject_Repr(attr(d, N.loop).get())).get());
         throw EncodeError{"decode references unknown loop " + r};
       }
       out.push_back(OP_VAR);
-      out.push_back(it->second);
+      out.push_back(*it);
       return;
     }
     case K_DCONST:
@@ -228,7 +253,8 @@ void walk_expr(PyObject* e, std::vector<PyObject*>& reads, int32_t* ops, std::ve
       reads.push_back(e);
       return;
     case K_BIN: {
-      std::string op = as_str(attr(e, N.op).get());
+      Ref opo = attr(e, N.op);
+      Str op = as_str(opo.get());
       int b = C_OTHER;
       if (op == "add") b = C_ADD;
       else if (op == "sub") b = C_SUB;
@@ -236,7 +262,7 @@ void walk_expr(PyObject* e, std::vector<PyObject*>& reads, int32_t* ops, std::ve
       else if (op == "div") b = C_DIV;
       else if (op == "max" || op == "min") b = C_MINMAX;
       else if (op == "lt" || op == "le" || op == "gt" || op == "ge" || op == "eq") b = C_CMP;
-      else throw EncodeError{"unknown binary op " + op};
+      else throw EncodeError{"unknown binary op " + std::string(op)};
       ops[b]++;
       Ref l = attr(e, N.lhs), r = attr(e, N.rhs);
       walk_expr(l.get(), reads, ops, keep);
@@ -293,7 +319,7 @@ class Encoder {
   int64_t encode_program(PyObject* p) {
     Seq stages_seq(attr(p, N.stages).get());
     std::vector<StageInfo> stages(stages_seq.n);
-    std::unordered_map<std::string, int> smap;
+    FlatMap<int> smap;
     for (Py_ssize_t i = 0; i < stages_seq.n; ++i) {
       PyObject* s = stages_seq.items[i];
       StageInfo& S = stages[i];
@@ -308,10 +334,10 @@ class Encoder {
         S.at_loop = as_str(t.items[1]);
       }
       if (!S.inlined) load_loops(S);
-      smap[S.name] = (int)i;      // dict: the last stage of a name wins
+      smap.set(S.name, (int)i);   // dict: the last stage of a name wins
     }
     // layouts: buffer -> descriptor (dim, extent) pairs
-    std::unordered_map<std::string, std::vector<std::pair<int, int64_t>>> layouts;
+    FlatMap<std::vector<std::pair<int, int64_t>>> layouts;
     {
       Seq lay(attr(p, N.layouts).get());
       for (Py_ssize_t i = 0; i < lay.n; ++i) {
@@ -322,13 +348,13 @@ class Encoder {
           Seq de(ds.items[j]);
           desc.emplace_back((int)as_i64(de.items[0]), as_i64(de.items[1]));
         }
-        layouts[as_str(kv.items[0])] = std::move(desc);
+        layouts.set(as_str(kv.items[0]), std::move(desc));
       }
     }
     int n_live = 0;
     for (auto& S : stages) n_live += S.inlined ? 0 : 1;
     Ref dag = attr(p, N.dag);
-    std::unordered_map<std::string, std::vector<int64_t>> node_shapes;
+    FlatMap<std::vector<int64_t>> node_shapes;
     int64_t emitted = 0;
     for (auto& S : stages) {
       if (S.inlined) continue;
@@ -340,25 +366,24 @@ class Encoder {
 
  private:
   void nest_above(const StageInfo& s, std::vector<StageInfo>& stages,
-                  const std::unordered_map<std::string, int>& smap, std::vector<const LoopInfo*>& out, int depth) {
+                  const FlatMap<int>& smap, std::vector<const LoopInfo*>& out, int depth) {
     if (!s.has_at) return;
     if (depth > 256) throw EncodeError{"compute_at cycle"};
-    auto it = smap.find(s.at_stage);
-    if (it == smap.end()) throw EncodeError{"compute_at references unknown stage " + s.at_stage};
-    StageInfo& t = stages[it->second];
+    const int* it = smap.find(s.at_stage);
+    if (!it) throw EncodeError{"compute_at references unknown stage " + std::string(s.at_stage)};
+    StageInfo& t = stages[*it];
     load_loops(t);
     nest_above(t, stages, smap, out, depth + 1);
     int upto = -1;
     for (size_t j = 0; j < t.loops.size(); ++j)
       if (t.loops[j].id == s.at_loop) { upto = (int)j; break; }       // list.index: first match
-    if (upto < 0) throw EncodeError{"compute_at references unknown loop " + s.at_loop};
+    if (upto < 0) throw EncodeError{"compute_at references unknown loop " + std::string(s.at_loop)};
     for (int j = 0; j <= upto; ++j) out.push_back(&t.loops[j]);
   }
 
   void encode_stage(const StageInfo& S, std::vector<StageInfo>& stages,
-                    const std::unordered_map<std::string, int>& smap,
-                    const std::unordered_map<std::string, std::vector<std::pair<int, int64_t>>>& layouts,
-                    int n_live, PyObject* dag, std::unordered_map<std::string, std::vector<int64_t>>& node_shapes) {
+                    const FlatMap<int>& smap, const FlatMap<std::vector<std::pair<int, int64_t>>>& layouts,
+                    int n_live, PyObject* dag, FlatMap<std::vector<int64_t>>& node_shapes) {
     PyObject* s = S.obj;
     std::vector<const LoopInfo*> above_all, above, nest;
     nest_above(S, stages, smap, above_all, 0);
@@ -367,40 +392,41 @@ class Encoder {
     nest = above;
     for (auto& l : S.loops)
       if (l.extent > 1) nest.push_back(&l);
-    std::unordered_map<std::string, int> loop_idx, last_pos;
-    for (size_t j = 0; j < S.loops.size(); ++j) loop_idx[S.loops[j].id] = (int)j;
-    for (size_t q = 0; q < nest.size(); ++q) last_pos[nest[q]->id] = (int)q;
+    FlatMap<int> loop_idx, last_pos;
+    for (size_t j = 0; j < S.loops.size(); ++j) loop_idx.set(S.loops[j].id, (int)j);
+    for (size_t q = 0; q < nest.size(); ++q) last_pos.set(nest[q]->id, (int)q);
 
     // index_map: iterator names in order, decode per name (dict: last wins)
     Seq imap(attr(s, N.index_map).get());
-    std::vector<std::string> iters;
-    std::unordered_map<std::string, PyObject*> dmap;
-    std::unordered_map<std::string, int> iter_idx;
+    std::vector<Str> iters;
+    FlatMap<PyObject*> dmap;
+    FlatMap<int> iter_idx;
+    std::vector<Seq> kvs;
+    kvs.reserve(imap.n);
     for (Py_ssize_t j = 0; j < imap.n; ++j) {
-      Seq kv(imap.items[j]);
-      std::string nm = as_str(kv.items[0]);
+      kvs.emplace_back(imap.items[j]);
+      Str nm = as_str(kvs.back().items[0]);
       iters.push_back(nm);
-      dmap[nm] = kv.items[1];
-      iter_idx[nm] = (int)j;
+      dmap.set(nm, kvs.back().items[1]);
+      iter_idx.set(nm, (int)j);
     }
     std::vector<int32_t> nodes, iter_tab;
     for (auto& nm : iters) {
       int start = (int)(nodes.size() / 2);
-      postfix(dmap[nm], loop_idx, nodes);
+      postfix(*dmap.find(nm), loop_idx, nodes);
       iter_tab.push_back(start);
       iter_tab.push_back((int)(nodes.size() / 2) - start);
     }
     int n_extra = 0;
-    auto iter_slot = [&](const std::string& name) -> int {
-      auto it = iter_idx.find(name);
-      if (it != iter_idx.end()) return it->second;
-      auto li = loop_idx.find(name);
-      if (li == loop_idx.end()) throw EncodeError{"iterator '" + name + "' has no decode and no loop"};
+    auto iter_slot = [&](Str name) -> int {
+      if (const int* it = iter_idx.find(name)) return *it;
+      const int* li = loop_idx.find(name);
+      if (!li) throw EncodeError{"iterator '" + std::string(name) + "' has no decode and no loop"};
       int slot = (int)iters.size() + n_extra++;
-      iter_idx[name] = slot;
+      iter_idx.set(name, slot);
       int start = (int)(nodes.size() / 2);
       nodes.push_back(OP_VAR);
-      nodes.push_back(li->second);
+      nodes.push_back(*li);
       iter_tab.push_back(start);
       iter_tab.push_back(1);
       return slot;
@@ -412,13 +438,13 @@ class Encoder {
     std::vector<Ref> keep;
     int32_t ops[N_KINDS] = {0};
     if (expr.get() != Py_None) walk_expr(expr.get(), rd, ops, keep);
-    std::unordered_map<std::string, int> vpos;
-    std::vector<std::string> order;
+    FlatMap<int> vpos;
+    std::vector<Str> order;
     std::vector<View> views;
-    auto access = [&](const std::string& buf, PyObject* index, int is_w) {
-      auto it = vpos.find(buf);
+    auto access = [&](Str buf, PyObject* index, int is_w) {
+      const int* it = vpos.find(buf);
       int vi;
-      if (it == vpos.end()) {
+      if (!it) {
         // logical (const, [(iter slot, coeff)]) per dim, iter_slot called in dim / term order
         std::vector<std::pair<int64_t, std::vector<std::pair<int, int64_t>>>> logical;
         if (index == nullptr) {
@@ -441,46 +467,45 @@ class Encoder {
           }
         }
         View V;
-        auto lay = layouts.find(buf);
-        if (lay != layouts.end()) {
-          const auto& desc = lay->second;
+        if (const auto* lay = layouts.find(buf)) {
+          const auto& desc = *lay;
           for (size_t i = 0; i < desc.size(); ++i) {
             int64_t st = 1;
             for (size_t i2 = i + 1; i2 < desc.size(); ++i2)
               if (desc[i2].first == desc[i].first) st *= desc[i2].second;
             int d = desc[i].first;
-            if (d < 0 || d >= (int)logical.size()) throw EncodeError{"layout dim out of range for " + buf};
+            if (d < 0 || d >= (int)logical.size()) throw EncodeError{"layout dim out of range for " + std::string(buf)};
             V.dims.push_back({desc[i].second, st, desc[i].second, logical[d].first, logical[d].second});
           }
         } else {
           const std::vector<int64_t>* shape = nullptr;
-          auto si = smap.find(buf);
-          if (si != smap.end()) {
-            load_loops(stages[si->second]);
-            shape = &stages[si->second].shape;
+          if (const int* si = smap.find(buf)) {
+            load_loops(stages[*si]);
+            shape = &stages[*si].shape;
           } else {
-            auto ns = node_shapes.find(buf);
-            if (ns == node_shapes.end()) {
+            const std::vector<int64_t>* ns = node_shapes.find(buf);
+            if (!ns) {
               Ref bname(PyUnicode_FromStringAndSize(buf.data(), (Py_ssize_t)buf.size()));
               Ref node(PyObject_CallMethodObjArgs(dag, N.node, bname.get(), nullptr));
               if (!node.get()) throw PyErrSet{};
               Seq sh(attr(node.get(), N.shape).get());
               std::vector<int64_t> v;
               for (Py_ssize_t d = 0; d < sh.n; ++d) v.push_back(as_i64(sh.items[d]));
-              ns = node_shapes.emplace(buf, std::move(v)).first;
+              node_shapes.set(buf, std::move(v));
+              ns = node_shapes.find(buf);
             }
-            shape = &ns->second;
+            shape = ns;
           }
-          if (shape->size() < logical.size()) throw EncodeError{"access rank exceeds the shape of " + buf};
+          if (shape->size() < logical.size()) throw EncodeError{"access rank exceeds the shape of " + std::string(buf)};
           for (size_t d = 0; d < logical.size(); ++d)
             V.dims.push_back({(*shape)[d], 1, 0, logical[d].first, logical[d].second});
         }
         vi = (int)views.size();
         views.push_back(std::move(V));
-        vpos[buf] = vi;
+        vpos.set(buf, vi);
         order.push_back(buf);
       } else {
-        vi = it->second;
+        vi = *it;
       }
       views[vi].n_marks += 1;
       views[vi].has_w |= is_w;
@@ -491,10 +516,10 @@ class Encoder {
       access(as_str(buf.get()), index.get(), 0);
     }
     access(S.name, nullptr, 1);
-    std::vector<std::string> sorted_names = order;
+    std::vector<Str> sorted_names = order;
     std::sort(sorted_names.begin(), sorted_names.end());
-    std::unordered_map<std::string, int> rank;
-    for (size_t r = 0; r < sorted_names.size(); ++r) rank[sorted_names[r]] = (int)r;
+    FlatMap<int> rank;
+    for (size_t r = 0; r < sorted_names.size(); ++r) rank.set(sorted_names[r], (int)r);
 
     // record
     std::vector<int32_t>& w = words;
@@ -510,25 +535,25 @@ class Encoder {
     for (int k = 0; k < N_KINDS; ++k) w.push_back(ops[k]);
     w.push_back((int32_t)(nodes.size() / 2));
     for (auto* l : nest) {
-      auto li = loop_idx.find(l->id);
+      const int* li = loop_idx.find(l->id);
       w.push_back((int32_t)l->extent);
       w.push_back(l->kind);
       w.push_back(l->ann);
-      w.push_back(li == loop_idx.end() ? -1 : li->second);
+      w.push_back(li ? *li : -1);
     }
     for (auto& l : S.loops) {
-      auto lp = last_pos.find(l.id);
+      const int* lp = last_pos.find(l.id);
       w.push_back((int32_t)l.extent);
       w.push_back(l.kind);
-      w.push_back(lp == last_pos.end() ? -1 : lp->second);
+      w.push_back(lp ? *lp : -1);
     }
     w.insert(w.end(), iter_tab.begin(), iter_tab.end());
     w.insert(w.end(), nodes.begin(), nodes.end());
     for (auto& b : order) {
-      const View& V = views[vpos[b]];
+      const View& V = views[*vpos.find(b)];
       w.push_back(V.n_marks);
       w.push_back(V.has_w);
-      w.push_back(rank[b]);
+      w.push_back(*rank.find(b));
       w.push_back((int32_t)V.dims.size());
       for (auto& d : V.dims) {
         w.push_back((int32_t)d.size);
