@@ -605,7 +605,7 @@ def main() -> None:
                         "kernels_compiled": stats.get("kernels_compiled", 0),
                         "kernels_shared": stats.get("kernels_shared", 0),
                         "mean_s": stats["compile_s"] / max(1, stats["compiled"])},
-            "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s")},
+            "pipeline_s": {k: round(stats[k], 3) for k in ("wall_s", "lower_s", "gpu_s", "load_s", "idle_s", "prep_s", "lt_measure_s") if k in stats},
             "roofline": found_roofline(args.config) or roofline(head),
             "roofline_stream_best": roofline(head),
             "e2e": {"value": e2e, "unit": "cand/s", "h2d_bytes_per_step": int(h2d_step),
