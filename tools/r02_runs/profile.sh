@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 ncu evidence, run on the GPU box:  bash tools/r02_profile.sh
+# Round-2 ncu evidence, run on the GPU box:  bash tools/r02_runs/profile.sh
 # (1) launch list of a short bench run: the candidates run in the measuring child
 #     process, hence --target-processes all (a number printed under ncu is never a bench value);
 # (2) one full capture per best-found program (profiles/r02_tuned_best.json);
