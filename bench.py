@@ -635,20 +635,24 @@ def main() -> None:
             tbytes = sb["n_stmt"] * sb["n_used"] * 8 + sb["n_stmt"] * 8
             hbm = peaks.get("hbm_gbs")
 
-            def hbm_roof(nbytes, ms, what):
+            def hbm_roof(nbytes, ms, what, kernel=""):
                 ach = nbytes / (ms / 1000) / 1e9
+                # DRAM bytes of this kernel on this same population from one ncu --set full
+                # capture (tools/profile_scoring.py, profiles/traffic.json "scoring:<kernel>")
+                tr = traffic_of(f"scoring:{kernel}") if kernel else None
                 return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                        "frac": ach / hbm if hbm else None, "traffic": None, "algorithmic_bytes": nbytes,
+                        "frac": ach / hbm if hbm else None, "traffic": tr, "algorithmic_bytes": nbytes,
                         "bytes_def": what, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
             line["scoring"] = {
                 "programs": sb["n_prog"], "statements": sb["n_stmt"],
                 "device_programs_per_s": sb["n_prog"] / ((sb["features_ms"] + sb["trees_ms"] + sb["segsum_ms"]) / 1000),
                 "e2e_programs_per_s": sb["n_prog"] / sb["e2e_s"],
                 "features_ms": sb["features_ms"], "trees_ms": sb["trees_ms"], "segsum_ms": sb["segsum_ms"],
-                "roofline_features": hbm_roof(fbytes, sb["features_ms"], "encoded words read + rows x 164 x 8 B written"),
+                "roofline_features": hbm_roof(fbytes, sb["features_ms"], "encoded words read + rows x 164 x 8 B written",
+                                              "features_kernel"),
                 "roofline_trees": hbm_roof(tbytes, sb["trees_ms"],
                                            f"rows x {sb['n_used']} used feature columns x 8 B read + rows x 8 B "
-                                           "written (the model is shared-memory resident)")}
+                                           "written (the model is shared-memory resident)", "predict_perfect_kernel")}
             line["train"] = train_bench()
         if not args.no_cpu:
             pool = RefPool(cores)

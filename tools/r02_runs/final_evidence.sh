@@ -25,6 +25,31 @@ for c in os.environ.get("CFGS", "RC CL G10 TBG").split():
     subprocess.run([sys.executable, "tools/ncu_summary.py", f"gpurun_out/c10_best_{c}.ncu-rep", "--header",
                     f"{c} ({src}): {head}", "--traffic-key", key, "--config", c], check=False)
 PY
+# scoring kernels on the bench's own population: DRAM bytes per launch -> traffic.json "scoring:<kernel>"
+timeout 600 ncu --set full --clock-control none --nvtx --nvtx-include "profile/" -c 3 -o gpurun_out/c10_scoring -f \
+    python tools/profile_scoring.py 1 > /dev/null 2>&1
+python tools/ncu_summary.py gpurun_out/c10_scoring.ncu-rep --header "population scoring, 65,536 programs (tools/profile_scoring.py)" \
+    > gpurun_out/c10_scoring_ncu.txt 2>&1
+python - <<'PY'
+import csv, io, json, subprocess
+out = subprocess.run(["ncu", "-i", "gpurun_out/c10_scoring.ncu-rep", "--page", "raw", "--csv", "--metrics",
+                      "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out[out.find('"'):])))
+h, units, body = rows[0], rows[1], rows[2:]
+ix = {k: i for i, k in enumerate(h)}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+data = json.load(open("profiles/traffic.json"))
+for r in body:
+    name = r[ix["Kernel Name"]].split("(")[0]
+    key = f"scoring:{name}"
+    if key in data and data[key].get("round") == "r02-final":
+        continue
+    tot = sum(float(r[ix[m]].replace(",", "")) * scale.get(units[ix[m]], 1)
+              for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    data[key] = {"config": "scoring", "dram_bytes_per_launch": tot, "round": "r02-final",
+                 "source": "ncu --set full --clock-control none, tools/profile_scoring.py 1 (65,536 programs)"}
+json.dump(data, open("profiles/traffic.json", "w"), indent=1)
+PY
 cp profiles/traffic.json gpurun_out/c10_traffic.json
 timeout 700 python bench.py > gpurun_out/c10_bench.json 2> gpurun_out/c10_bench.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --target-processes all -c 4000 --csv \
