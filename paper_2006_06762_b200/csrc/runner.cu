@@ -240,20 +240,6 @@ int lt_function_info(int64_t func, int* regs, int* local_bytes, int* max_threads
 
 int64_t lt_task_create(int device) {
   if (lt::check_cuda(cudaSetDevice(device), "cudaSetDevice")) return 0;
-  // Keep the local-memory reservation at its high-water mark: by default the driver
-  // shrinks it again after a launch that grew it, so every spilling candidate paid
-  // a device-synchronising reallocation per launch (LT_LMEM_SHRINK=1 restores that).
-  static bool lmem_set[64] = {};
-  if (device >= 0 && device < 64 && !lmem_set[device]) {
-    lmem_set[device] = true;
-    const char* e = getenv("LT_LMEM_SHRINK");
-    if (!(e && e[0] == '1')) {
-      unsigned int fl = 0;
-      cudaGetDeviceFlags(&fl);
-      cudaSetDeviceFlags((fl & ~cudaDeviceMapHost) | cudaDeviceLmemResizeToMax);
-      cudaGetLastError();
-    }
-  }
   Task* t = new Task();
   t->device = device;
   if (lt::check_cuda(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking), "stream") ||
