@@ -18,6 +18,7 @@
 #include <cstring>
 #include <string>
 #include <string_view>
+#include <functional>
 #include <unordered_map>
 #include <utility>
 #include <vector>
@@ -88,15 +89,26 @@ int64_t as_i64(PyObject* o) {
   return v;
 }
 
-// UTF-8 view of a str attribute; the objects it points into are owned by the
-// programs being encoded, which the caller keeps alive for the whole call
-using Str = std::string_view;
+// UTF-8 view of a str attribute plus its (cached) Python hash; the objects it points
+// into are owned by the programs being encoded, which the caller keeps alive for the
+// whole call.  Equality tests the hash first, so the small linear maps below cost an
+// integer compare per entry.
+struct Str {
+  std::string_view v;
+  Py_hash_t h = 0;
+  bool operator==(const Str& o) const { return h == o.h && v == o.v; }
+  bool operator==(const char* lit) const { return v == lit; }
+  bool operator<(const Str& o) const { return v < o.v; }
+  explicit operator std::string() const { return std::string(v); }
+};
 
 Str as_str(PyObject* o) {
   Py_ssize_t n;
   const char* s = PyUnicode_AsUTF8AndSize(o, &n);
   if (!s) throw PyErrSet{};
-  return Str(s, (size_t)n);
+  Py_hash_t h = PyObject_Hash(o);
+  if (h == -1) throw PyErrSet{};
+  return Str{std::string_view(s, (size_t)n), h};
 }
 
 // small insertion-ordered map with dict assignment semantics (d[k] = v overwrites)
@@ -485,7 +497,7 @@ class Encoder {
           } else {
             const std::vector<int64_t>* ns = node_shapes.find(buf);
             if (!ns) {
-              Ref bname(PyUnicode_FromStringAndSize(buf.data(), (Py_ssize_t)buf.size()));
+              Ref bname(PyUnicode_FromStringAndSize(buf.v.data(), (Py_ssize_t)buf.v.size()));
               Ref node(PyObject_CallMethodObjArgs(dag, N.node, bname.get(), nullptr));
               if (!node.get()) throw PyErrSet{};
               Seq sh(attr(node.get(), N.shape).get());
