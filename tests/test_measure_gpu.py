@@ -301,3 +301,24 @@ def test_device_packing_equals_host_pack():
         finally:
             core.close()
     assert seen >= 10
+
+
+def test_states_both_ptx_builds_get_wrong_are_measured_through_nvrtc():
+    """Register-overflowing tiles whose PTX is assembled wrongly at both ptxas levels
+    (tests/golden/ptx_rejected_states.json, found by tools/invalid_probe.py) are legal
+    States: the runner re-lowers them to CUDA C, compiles with NVRTC, verifies again
+    and reports them VALID, as the reference does."""
+    from paper_2006_06762_b200 import measure, resnet50
+    from paper_2006_06762_b200.state import history_from_json, replay
+    data = json.load(open(os.path.join(GOLDEN, "ptx_rejected_states.json")))
+    dags = {n: d for n, d, _ in resnet50.tasks()}
+    core = measure.RunnerCore(device=0, cache_dir="")
+    try:
+        progs = [replay(dags[s["task"]], history_from_json(s["history"])) for s in data["states"]]
+        recs = [core.measure_programs([p])[0] for p in progs]
+    finally:
+        core.close()
+    for s, r in zip(data["states"], recs):
+        assert r.status == "valid", (s["task"], s["i"], r.detail)
+        assert r.max_rel_err <= 1e-4
+        assert r.cost_us > 0 and math.isfinite(r.cost_us)
